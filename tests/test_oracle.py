@@ -1,0 +1,99 @@
+"""The CPU oracle reproduces the reference bit for bit on its own outputs.
+
+Fixtures in tests/golden were produced by running the reference
+(/root/reference/pkg/src/isoclust, pinned numpy mode) via tools/gen_golden.py.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_pipeline_cases, load, random_instance_trees
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+@pytest.mark.parametrize("path", golden_pipeline_cases(), ids=lambda p: p.rsplit("/", 1)[-1])
+def test_oracle_pipeline_matches_reference(path, oracle_mod):
+    g = load(path)
+    n, d, k, seed = int(g["n"]), int(g["d"]), int(g["k"]), int(g["seed"])
+    pts, _ = oracle_mod.generate_random(n, d, k, seed)
+    # distances: first and last row bitwise (scipy order)
+    assert np.array_equal(bits(oracle_mod.distance_rows(pts, 0, 1)[0]), bits(g["row0"]))
+    assert np.array_equal(bits(oracle_mod.distance_rows(pts, n - 1, n)[0]), bits(g["rowlast"]))
+    assert oracle_mod.flat_distance_sum(pts) == float(g["dsum"])
+    sigma = "auto" if float(g["sigma_arg"]) < 0 else float(g["sigma_arg"])
+    out = oracle_mod.run_pipeline(pts, k, sigma=sigma, alpha=float(g["alpha"]), root=int(g["root"]))
+    assert out.sigma == float(g["sigma"])
+    t = out.tree
+    for name in ("parent", "depth", "child_id", "bfs_order"):
+        assert np.array_equal(getattr(t, name), g[name]), name
+    assert np.array_equal(bits(t.parent_flow), bits(g["parent_flow"]))
+    assert math.fsum(t.parent_dist) == float(g["total_distance"])
+    assert np.array_equal(bits(out.omega), bits(g["omega"]))
+    assert np.array_equal(bits(out.p), bits(g["p"]))
+    e = out.extrema
+    assert [e.phi_star_sum, e.phi_star_min, e.omega_star_sum, e.omega_star_min, e.p_star_sum,
+            e.p_star_min] == list(g["extrema"])
+    r = out.result
+    assert np.array_equal(r.labels, g["labels"])
+    assert r.miso == float(g["miso"])
+    assert r.iterations == int(g["iterations"])
+    assert r.alpha_final == float(g["alpha_final"]) and r.beta_final == float(g["beta_final"])
+    assert [m for m, _ in r.trace] == list(g["trace_mid"])
+    assert [int(f) for _, f in r.trace] == list(g["trace_ok"])
+    assert np.array_equal(r.outcome.cut, g["cut"]) and np.array_equal(r.outcome.eta, g["eta"])
+    assert r.outcome.cluster_sparsities == list(g["sparsities"])
+
+
+def test_oracle_tree_phase_matches_reference(oracle_mod):
+    for rec in random_instance_trees():
+        k = int(rec["k"])
+        if not int(rec["ok"]):
+            with pytest.raises(oracle_mod.InfeasibleSubpartitionError):
+                oracle_mod.solve_tree(rec["parent"], rec["flows"], rec["omega"], rec["p"], k)
+            continue
+        res, tree, _ = oracle_mod.solve_tree(rec["parent"], rec["flows"], rec["omega"], rec["p"], k)
+        assert np.array_equal(tree.child_id, rec["child_id"])
+        assert np.array_equal(tree.bfs_order, rec["bfs_order"])
+        assert np.array_equal(res.labels, rec["labels"])
+        assert res.miso == float(rec["miso"])
+        assert res.iterations == int(rec["iterations"])
+        assert [m for m, _ in res.trace] == list(rec["trace_mid"])
+        assert res.outcome.cluster_sparsities == list(rec["sparsities"])
+
+
+def test_oracle_rrt_20000(oracle_mod):
+    import os
+    from conftest import GOLDEN
+    g = load(os.path.join(GOLDEN, "tree_rrt_n20000_k20.npz"))
+    res, tree, _ = oracle_mod.solve_tree(g["parent"], g["flows"], g["omega"], g["p"], int(g["k"]))
+    assert np.array_equal(tree.bfs_order, g["bfs_order"])
+    assert np.array_equal(res.labels, g["labels"])
+    assert res.miso == float(g["miso"]) and res.iterations == int(g["iterations"])
+    assert res.alpha_final == float(g["alpha_final"]) and res.beta_final == float(g["beta_final"])
+
+
+def test_oracle_exp_matches_libm(oracle_mod):
+    # the pinned-mode np.exp is glibc exp: compare against libm directly
+    import ctypes
+    libm = ctypes.CDLL("libm.so.6")
+    libm.exp.restype = ctypes.c_double
+    libm.exp.argtypes = [ctypes.c_double]
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([-rng.random(20000) * 40, -rng.random(2000) * 800, (rng.random(2000) - 0.5) * 1500,
+                         [0.0, -0.0, -1e-300, -745.2, -708.4, -709.9, 709.7, -1e-17]])
+    got = oracle_mod.exp(xs)
+    want = np.array([libm.exp(float(x)) for x in xs])
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+def test_pairwise_sum_matches_numpy(oracle_mod):
+    rng = np.random.default_rng(9)
+    for n in (0, 1, 7, 8, 9, 127, 128, 129, 1000, 8193, 123457):
+        a = rng.random(n) * 100
+        assert oracle_mod.pairwise_sum(a) == float(np.sum(a))
