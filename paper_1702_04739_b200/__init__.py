@@ -1,0 +1,51 @@
+"""paper_1702_04739_b200: B200-native isoperimetric-tree clustering.
+
+Drop-in for the clustering path of the reference package `isoclust`
+(/root/reference/pkg/src/isoclust, arXiv 1702.04739): `run_pipeline(points,
+k, ...)` returns the same PipelineRun / MisoResult structures, bit-exact
+labels, and runs every arithmetic stage as hand-written sm_100a CUDA kernels
+behind the C ABI in include/isoclust_b200.h (libisoclust_b200.so).
+"""
+from ._lib import InfeasibleSubpartitionError
+from .pipeline import (
+    ENGINES,
+    WORKERS_ENV_VAR,
+    auto_sigma,
+    decide,
+    extrema,
+    minimum_spanning_tree,
+    node_weights,
+    par_decide,
+    par_solve_miso,
+    prim_mst,
+    resolve_workers,
+    run_pipeline,
+    solve_miso,
+    summarize,
+    total_distance,
+    tree_from_parent_list,
+)
+from .types import (
+    BRACKET_EPS,
+    MAX_ITERATIONS,
+    NO_VERTEX,
+    DecisionOutcome,
+    Extrema,
+    MisoResult,
+    NodeWeights,
+    PipelineRun,
+    RootedTree,
+    miso_results_equal,
+    outcomes_equal,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BRACKET_EPS", "DecisionOutcome", "ENGINES", "Extrema", "InfeasibleSubpartitionError",
+    "MAX_ITERATIONS", "MisoResult", "NO_VERTEX", "NodeWeights", "PipelineRun", "RootedTree",
+    "WORKERS_ENV_VAR", "auto_sigma", "decide", "extrema", "minimum_spanning_tree",
+    "miso_results_equal", "node_weights", "outcomes_equal", "par_decide", "par_solve_miso",
+    "prim_mst", "resolve_workers", "run_pipeline", "solve_miso", "summarize", "total_distance",
+    "tree_from_parent_list", "__version__",
+]

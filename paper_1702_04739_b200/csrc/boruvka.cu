@@ -1,0 +1,534 @@
+// Boruvka MST rounds on the complete Euclidean graph (replaces prim_mst,
+// /root/reference/pkg/src/isoclust/mst.py:128-181).
+//
+// Edge order is the lexicographic key (d_exact, min(u,v), max(u,v)); with
+// distinct exact distances the resulting edge set is the unique MST that Prim
+// returns.  Per round:
+//   1. boruvka_filter_kernel: FP32 Gram-form FFMA tiles (centred data) with
+//      a fused per-row arg-min epilogue over columns in other components:
+//      best approximate value a1 (column j1) and second best a2.
+//   2. certified selection: |a - d_exact^2| <= E_i (rigorous FP32 bound, see
+//      DESIGN.md); rows that cannot hold their component's minimum are
+//      dropped, rows with a unique candidate get one exact fp64 distance,
+//      ambiguous rows are rescanned exactly.
+//   3. per-component exact minimum (two 64-bit atomicMin phases: weight bits,
+//      then packed endpoints), hooking with mutual-pair resolution, pointer
+//      jumping.  The 64-bit keys are what the multi-GPU path all-reduces.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace isoc {
+
+constexpr int FM = 128, FN = 128, FK = 8, FT = 256;
+// "no edge" sentinel: INT64_MAX, so keys also order correctly as signed
+// int64 (NCCL/torch MIN all-reduce); weight bits of positive doubles and
+// packed endpoint pairs are all below 2^63.
+constexpr unsigned long long kNoKey = 0x7fffffffffffffffull;
+
+__global__ void fill_u64_kernel(unsigned long long* v, int64_t m, unsigned long long x) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) v[i] = x;
+}
+
+struct FilterSmem {
+    float As[2][FK][FM];
+    float Bs[2][FK][FN];
+    float red_a1[16][FM];
+    float red_a2[16][FM];
+    int32_t red_j1[16][FM];
+};
+
+__device__ __forceinline__ void approx_update(float a, int32_t j, float& a1, int32_t& j1, float& a2) {
+    const bool lt = a < a1;
+    a2 = fminf(a2, fmaxf(a, a1));
+    j1 = lt ? j : j1;
+    a1 = fminf(a1, a);
+}
+
+// Y: n x dp fp32 (dp % 8 == 0), ny: |y|^2 fp32, comp: component ids.
+__global__ void __launch_bounds__(FT, 1)
+boruvka_filter_kernel(const float* __restrict__ Y, const float* __restrict__ ny,
+                      const int32_t* __restrict__ comp, int64_t n, int dp, int64_t row_lo,
+                      int64_t row_hi, float* __restrict__ out_a1, int32_t* __restrict__ out_j1,
+                      float* __restrict__ out_a2) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FilterSmem& sm = *reinterpret_cast<FilterSmem*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int64_t r0 = row_lo + (int64_t)blockIdx.x * FM;
+
+    // thread rows: ty*4+{0..3}, 64+ty*4+{0..3}; cols: tx*4+{0..3}, 64+tx*4+{0..3}
+    int64_t rows[8];
+    int32_t rc[8];
+    float rn[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        rows[i] = r0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        const bool ok = rows[i] < row_hi;
+        rc[i] = ok ? comp[rows[i]] : -2;
+        rn[i] = ok ? ny[rows[i]] : 0.f;
+    }
+    float a1[8], a2[8];
+    int32_t j1[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { a1[i] = INFINITY; a2[i] = INFINITY; j1[i] = -1; }
+
+    // global->smem mapping: each thread loads one float4 of A and one of B
+    const int lrow = tid >> 1, lk = (tid & 1) * 4;
+    const int nk = dp / FK;
+    const int64_t ntiles = (n + FN - 1) / FN;
+    for (int64_t t = 0; t < ntiles; ++t) {
+        const int64_t c0 = t * FN;
+        float acc[8][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+        auto load = [&](int kc, int buf) {
+            const int64_t ar = r0 + lrow, bc = c0 + lrow;
+            float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
+            if (ar < row_hi) va = *reinterpret_cast<const float4*>(Y + ar * dp + kc * FK + lk);
+            if (bc < n) vb = *reinterpret_cast<const float4*>(Y + bc * dp + kc * FK + lk);
+            sm.As[buf][lk + 0][lrow] = va.x; sm.As[buf][lk + 1][lrow] = va.y;
+            sm.As[buf][lk + 2][lrow] = va.z; sm.As[buf][lk + 3][lrow] = va.w;
+            sm.Bs[buf][lk + 0][lrow] = vb.x; sm.Bs[buf][lk + 1][lrow] = vb.y;
+            sm.Bs[buf][lk + 2][lrow] = vb.z; sm.Bs[buf][lk + 3][lrow] = vb.w;
+        };
+        __syncthreads();
+        load(0, 0);
+        __syncthreads();
+        for (int kc = 0; kc < nk; ++kc) {
+            const int buf = kc & 1;
+            if (kc + 1 < nk) load(kc + 1, buf ^ 1);
+#pragma unroll
+            for (int kk = 0; kk < FK; ++kk) {
+                const float4 a_lo = *reinterpret_cast<const float4*>(&sm.As[buf][kk][ty * 4]);
+                const float4 a_hi = *reinterpret_cast<const float4*>(&sm.As[buf][kk][64 + ty * 4]);
+                const float4 b_lo = *reinterpret_cast<const float4*>(&sm.Bs[buf][kk][tx * 4]);
+                const float4 b_hi = *reinterpret_cast<const float4*>(&sm.Bs[buf][kk][64 + tx * 4]);
+                const float av[8] = {a_lo.x, a_lo.y, a_lo.z, a_lo.w, a_hi.x, a_hi.y, a_hi.z, a_hi.w};
+                const float bv[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+            }
+            __syncthreads();
+        }
+        // epilogue: approximate squared distance, other-component arg-min
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t col = c0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+            const bool cok = col < n;
+            const int32_t cc = cok ? comp[col] : -3;
+            const float cn = cok ? ny[col] : 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float a = fmaf(-2.f, acc[i][j], rn[i] + cn);
+                a = (cc != rc[i] && cok) ? a : INFINITY;
+                approx_update(a, (int32_t)col, a1[i], j1[i], a2[i]);
+            }
+        }
+    }
+    // reduce across the 16 column groups
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int lr = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+        sm.red_a1[tx][lr] = a1[i];
+        sm.red_a2[tx][lr] = a2[i];
+        sm.red_j1[tx][lr] = j1[i];
+    }
+    __syncthreads();
+    if (tid < FM) {
+        const int64_t row = r0 + tid;
+        float b1 = INFINITY, b2 = INFINITY;
+        int32_t bj = -1;
+        for (int g = 0; g < 16; ++g) {
+            const float x1 = sm.red_a1[g][tid], x2 = sm.red_a2[g][tid];
+            const int32_t xj = sm.red_j1[g][tid];
+            const bool first = (x1 < b1) || (x1 == b1 && xj >= 0 && (bj < 0 || xj < bj));
+            if (first) {
+                b2 = fminf(x2, b1);
+                b1 = x1;
+                bj = xj;
+            } else {
+                b2 = fminf(b2, x1);
+            }
+        }
+        if (row < row_hi) {
+            out_a1[row - row_lo] = b1;
+            out_j1[row - row_lo] = bj;
+            out_a2[row - row_lo] = b2;
+        }
+    }
+}
+
+// Centre, round to fp32, pad to dp; norms in the same FFMA order as the dot
+// products; R_i = |y_i| rounded up, for the error bound.
+__global__ void prep_fp32_kernel(const double* __restrict__ X, const double* __restrict__ centre,
+                                 int64_t n, int d, int dp, float* __restrict__ Y,
+                                 float* __restrict__ ny, float* __restrict__ rad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float s = 0.f;
+    double r2 = 0.0;
+    for (int k = 0; k < dp; ++k) {
+        float y = 0.f;
+        if (k < d) y = (float)(X[i * d + k] - centre[k]);
+        Y[i * dp + k] = y;
+        s = fmaf(y, y, s);
+        r2 += (double)y * (double)y;
+    }
+    ny[i] = s;
+    rad[i] = __double2float_ru(sqrt(r2) * (1.0 + 1e-12));
+}
+
+__global__ void column_mean_kernel(const double* __restrict__ X, int64_t n, int d,
+                                   double* __restrict__ centre) {
+    // one block per dimension; any deterministic mean works (it only
+    // conditions the fp32 filter, the bound covers its rounding)
+    const int k = blockIdx.x;
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += X[i * d + k];
+    __shared__ double red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+        if ((int)threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) centre[k] = red[0] / (double)n;
+}
+
+__global__ void max_float_kernel(const float* __restrict__ v, int64_t n, uint32_t* __restrict__ out) {
+    float m = 0.f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = fmaxf(m, v[i]);
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// ------------------------------------------------------------ selection
+__device__ __forceinline__ float row_bound(float Ri, float Rmax, float cd) {
+    const float s = __fadd_ru(Ri, Rmax);
+    return __fmul_ru(cd, __fmul_ru(s, s));
+}
+
+__global__ void comp_bound_kernel(const float* __restrict__ a1, const float* __restrict__ rad,
+                                  const int32_t* __restrict__ comp, int64_t lo, int64_t hi,
+                                  const uint32_t* __restrict__ rmax_bits, float cd,
+                                  uint32_t* __restrict__ compB) {
+    const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hi) return;
+    const float v = a1[i - lo];
+    if (!(v < INFINITY)) return;
+    const float E = row_bound(rad[i], __uint_as_float(*rmax_bits), cd);
+    atomicMin(&compB[comp[i]], float_to_ordered(__fadd_ru(v, E)));
+}
+
+// Rows that may hold their component's minimum: certified rows get one exact
+// distance; ambiguous rows are queued for an exact rescan.
+__global__ void candidate_kernel(const double* __restrict__ X, int d, const float* __restrict__ a1,
+                                 const int32_t* __restrict__ j1, const float* __restrict__ a2,
+                                 const float* __restrict__ rad, const int32_t* __restrict__ comp,
+                                 int64_t lo, int64_t hi, const uint32_t* __restrict__ rmax_bits,
+                                 float cd, const uint32_t* __restrict__ compB,
+                                 double* __restrict__ cand_d, int32_t* __restrict__ cand_j,
+                                 int8_t* __restrict__ cand_state, int32_t* __restrict__ rescan_list,
+                                 int32_t* __restrict__ rescan_count) {
+    const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hi) return;
+    const int64_t li = i - lo;
+    cand_state[li] = 0;
+    const float v = a1[li];
+    if (!(v < INFINITY)) return;
+    const float E = row_bound(rad[i], __uint_as_float(*rmax_bits), cd);
+    const float B = ordered_to_float(compB[comp[i]]);
+    if (__fsub_rd(v, E) > B) return;
+    if (__fsub_rd(a2[li], E) > __fadd_ru(v, E)) {
+        const int32_t j = j1[li];
+        cand_d[li] = exact_dist(X + i * d, X + (int64_t)j * d, d);
+        cand_j[li] = j;
+        cand_state[li] = 1;
+    } else {
+        cand_state[li] = 2;
+        const int32_t slot = atomicAdd(rescan_count, 1);
+        rescan_list[slot] = (int32_t)i;
+    }
+}
+
+// Exact rescan of one row per CTA: min (d, j) over other-component columns,
+// plus whether the minimum is attained twice.
+__global__ void rescan_kernel(const double* __restrict__ X, int64_t n, int d,
+                              const int32_t* __restrict__ comp, int64_t lo,
+                              const int32_t* __restrict__ rescan_list,
+                              const int32_t* __restrict__ rescan_count, double* __restrict__ cand_d,
+                              int32_t* __restrict__ cand_j, int8_t* __restrict__ cand_tie) {
+    const int32_t cnt = *rescan_count;
+    for (int32_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+        const int64_t i = rescan_list[q];
+        const int32_t ci = comp[i];
+        double m1 = INFINITY, m2 = INFINITY;
+        int64_t bj = -1;
+        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+            if (comp[j] == ci) continue;
+            const double v = exact_dist(X + i * d, X + j * d, d);
+            if (v < m1) { m2 = m1; m1 = v; bj = j; }
+            else m2 = fmin(m2, v);
+        }
+        __shared__ double s1[256], s2[256];
+        __shared__ int64_t sj[256];
+        s1[threadIdx.x] = m1; s2[threadIdx.x] = m2; sj[threadIdx.x] = bj;
+        __syncthreads();
+        for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+            if ((int)threadIdx.x < off) {
+                const int o = threadIdx.x + off;
+                const bool first = (s1[o] < s1[threadIdx.x]) ||
+                                   (s1[o] == s1[threadIdx.x] && sj[o] >= 0 &&
+                                    (sj[threadIdx.x] < 0 || sj[o] < sj[threadIdx.x]));
+                if (first) {
+                    s2[threadIdx.x] = fmin(s2[o], s1[threadIdx.x]);
+                    s1[threadIdx.x] = s1[o];
+                    sj[threadIdx.x] = sj[o];
+                } else {
+                    s2[threadIdx.x] = fmin(s2[threadIdx.x], s1[o]);
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            cand_d[i - lo] = s1[0];
+            cand_j[i - lo] = (int32_t)sj[0];
+            cand_tie[i - lo] = (int8_t)(s2[0] == s1[0]);
+        }
+        __syncthreads();
+    }
+}
+
+// Round 1 from the fused exact nearest neighbours: every row is a candidate.
+__global__ void nn_candidates_kernel(const int32_t* __restrict__ nn_j, const double* __restrict__ nn_d,
+                                     const int8_t* __restrict__ nn_tie, int64_t rows,
+                                     double* __restrict__ cand_d, int32_t* __restrict__ cand_j,
+                                     int8_t* __restrict__ cand_state, int8_t* __restrict__ cand_tie) {
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= rows) return;
+    cand_d[li] = nn_d[li];
+    cand_j[li] = nn_j[li];
+    cand_state[li] = 1;
+    cand_tie[li] = nn_tie[li];
+}
+
+__global__ void comp_exact_min_kernel(const double* __restrict__ cand_d,
+                                      const int8_t* __restrict__ cand_state,
+                                      const int32_t* __restrict__ comp, int64_t lo, int64_t hi,
+                                      unsigned long long* __restrict__ compD) {
+    const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hi) return;
+    if (!cand_state[i - lo]) return;
+    atomicMin(&compD[comp[i]], (unsigned long long)__double_as_longlong(cand_d[i - lo]));
+}
+
+__device__ __forceinline__ unsigned long long pack_edge(int64_t a, int64_t b) {
+    const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+    return (unsigned long long)((lo << 32) | hi);
+}
+
+__global__ void comp_edge_kernel(const double* __restrict__ cand_d, const int32_t* __restrict__ cand_j,
+                                 const int8_t* __restrict__ cand_state,
+                                 const int32_t* __restrict__ comp, int64_t lo, int64_t hi,
+                                 const unsigned long long* __restrict__ compD,
+                                 unsigned long long* __restrict__ compE) {
+    const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hi) return;
+    const int64_t li = i - lo;
+    if (!cand_state[li]) return;
+    const int32_t c = comp[i];
+    if ((unsigned long long)__double_as_longlong(cand_d[li]) != compD[c]) return;
+    atomicMin(&compE[c], pack_edge(i, cand_j[li]));
+}
+
+// Exact ties at a component's minimum weight (a different edge, or a row
+// whose own minimum is attained twice) make the MST possibly non-unique.
+__global__ void comp_tie_kernel(const double* __restrict__ cand_d, const int32_t* __restrict__ cand_j,
+                                const int8_t* __restrict__ cand_state, const int8_t* __restrict__ cand_tie,
+                                const int32_t* __restrict__ comp, int64_t lo, int64_t hi,
+                                const unsigned long long* __restrict__ compD,
+                                const unsigned long long* __restrict__ compE,
+                                int32_t* __restrict__ ties) {
+    const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hi) return;
+    const int64_t li = i - lo;
+    if (!cand_state[li]) return;
+    const int32_t c = comp[i];
+    if ((unsigned long long)__double_as_longlong(cand_d[li]) != compD[c]) return;
+    if (pack_edge(i, cand_j[li]) != compE[c] || cand_tie[li]) atomicAdd(ties, 1);
+}
+
+// succ[c] = component on the other side of c's minimum edge (reps only).
+__global__ void hook_kernel(const int32_t* __restrict__ comp, int64_t n,
+                            const unsigned long long* __restrict__ compE, int32_t* __restrict__ succ) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    if (comp[c] != c) return;  // not a representative
+    const unsigned long long e = compE[c];
+    if (e == kNoKey) { succ[c] = (int32_t)c; return; }
+    const int64_t a = (int64_t)(e >> 32), b = (int64_t)(e & 0xffffffffull);
+    const int32_t ca = comp[a], cb = comp[b];
+    succ[c] = (ca == c) ? cb : ca;
+}
+
+// Mutual pairs: the smaller representative becomes the root; every other
+// hooked representative contributes its edge once.
+__global__ void resolve_emit_kernel(const int32_t* __restrict__ comp, int64_t n,
+                                    const unsigned long long* __restrict__ compE,
+                                    const unsigned long long* __restrict__ compD,
+                                    int32_t* __restrict__ succ, int32_t* __restrict__ succ2,
+                                    int32_t* __restrict__ eu, int32_t* __restrict__ ev,
+                                    double* __restrict__ ed, int32_t* __restrict__ ecount) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    if (comp[c] != c) return;
+    int32_t s = succ[c];
+    if (s != c && succ[s] == c && c < s) s = (int32_t)c;
+    succ2[c] = s;
+    if (s != c) {
+        const unsigned long long e = compE[c];
+        const int32_t slot = atomicAdd(ecount, 1);
+        eu[slot] = (int32_t)(e >> 32);
+        ev[slot] = (int32_t)(e & 0xffffffffull);
+        ed[slot] = __longlong_as_double((long long)compD[c]);
+    }
+}
+
+__global__ void jump_kernel(const int32_t* __restrict__ comp, int64_t n, int32_t* __restrict__ succ,
+                            int32_t* __restrict__ changed) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    if (comp[c] != c) return;
+    const int32_t s = succ[c], ss = succ[s];
+    if (s != ss) {
+        succ[c] = ss;
+        *changed = 1;
+    }
+}
+
+__global__ void relabel_kernel(int32_t* __restrict__ comp, int64_t n, const int32_t* __restrict__ succ,
+                               int32_t* __restrict__ nroots) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t c = comp[i];
+    const int32_t r = succ[c];
+    comp[i] = r;
+    if (i == r) atomicAdd(nroots, 1);
+}
+
+// ------------------------------------------------------------ launchers
+static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, double* centre, float* Y,
+                             float* ny, float* rad, uint32_t* rmax_bits, cudaStream_t st) {
+    column_mean_kernel<<<d, 256, 0, st>>>(X, n, d, centre);
+    prep_fp32_kernel<<<blocks_for(n, 256), 256, 0, st>>>(X, centre, n, d, dp, Y, ny, rad);
+    cudaMemsetAsync(rmax_bits, 0, sizeof(uint32_t), st);
+    max_float_kernel<<<296, 256, 0, st>>>(rad, n, rmax_bits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_boruvka_filter(const float* Y, const float* ny, const int32_t* comp, int64_t n,
+                                  int dp, int64_t lo, int64_t hi, float* a1, int32_t* j1, float* a2,
+                                  cudaStream_t st) {
+    if (hi <= lo) return cudaSuccess;
+    const size_t smem = sizeof(FilterSmem);
+    cudaError_t e = cudaFuncSetAttribute(boruvka_filter_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    boruvka_filter_kernel<<<blocks_for(hi - lo, FM), FT, smem, st>>>(Y, ny, comp, n, dp, lo, hi, a1,
+                                                                       j1, a2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float* a1,
+                                  const int32_t* j1, const float* a2, const float* rad,
+                                  const uint32_t* rmax_bits, float cd, const int32_t* comp,
+                                  int64_t lo, int64_t hi, uint32_t* compB, double* cand_d,
+                                  int32_t* cand_j, int8_t* cand_state, int8_t* cand_tie,
+                                  int32_t* rescan_list, int32_t* rescan_count, cudaStream_t st) {
+    const int64_t rows = hi - lo;
+    if (rows <= 0) return cudaSuccess;
+    cudaMemsetAsync(compB, 0xff, (size_t)n * sizeof(uint32_t), st);
+    cudaMemsetAsync(rescan_count, 0, sizeof(int32_t), st);
+    cudaMemsetAsync(cand_tie, 0, (size_t)rows, st);
+    comp_bound_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(a1, rad, comp, lo, hi, rmax_bits, cd,
+                                                              compB);
+    candidate_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(X, d, a1, j1, a2, rad, comp, lo, hi,
+                                                             rmax_bits, cd, compB, cand_d, cand_j,
+                                                             cand_state, rescan_list, rescan_count);
+    rescan_kernel<<<592, 256, 0, st>>>(X, n, d, comp, lo, rescan_list, rescan_count, cand_d, cand_j,
+                                       cand_tie);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nn_candidates(const int32_t* nn_j, const double* nn_d, const int8_t* nn_tie,
+                                 int64_t rows, double* cand_d, int32_t* cand_j, int8_t* cand_state,
+                                 int8_t* cand_tie, cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    nn_candidates_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(nn_j, nn_d, nn_tie, rows, cand_d,
+                                                                 cand_j, cand_state, cand_tie);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_comp_exact_min(const double* cand_d, const int8_t* cand_state,
+                                  const int32_t* comp, int64_t n, int64_t lo, int64_t hi,
+                                  unsigned long long* compD, cudaStream_t st) {
+    fill_u64_kernel<<<blocks_for(n, 256), 256, 0, st>>>(compD, n, kNoKey);
+    if (hi > lo)
+        comp_exact_min_kernel<<<blocks_for(hi - lo, 256), 256, 0, st>>>(cand_d, cand_state, comp, lo,
+                                                                         hi, compD);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_comp_edge(const double* cand_d, const int32_t* cand_j, const int8_t* cand_state,
+                             const int32_t* comp, int64_t n, int64_t lo, int64_t hi,
+                             const unsigned long long* compD, unsigned long long* compE,
+                             cudaStream_t st) {
+    fill_u64_kernel<<<blocks_for(n, 256), 256, 0, st>>>(compE, n, kNoKey);
+    if (hi > lo)
+        comp_edge_kernel<<<blocks_for(hi - lo, 256), 256, 0, st>>>(cand_d, cand_j, cand_state, comp,
+                                                                    lo, hi, compD, compE);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_comp_ties(const double* cand_d, const int32_t* cand_j, const int8_t* cand_state,
+                             const int8_t* cand_tie, const int32_t* comp, int64_t lo, int64_t hi,
+                             const unsigned long long* compD, const unsigned long long* compE,
+                             int32_t* ties, cudaStream_t st) {
+    if (hi > lo)
+        comp_tie_kernel<<<blocks_for(hi - lo, 256), 256, 0, st>>>(cand_d, cand_j, cand_state,
+                                                                   cand_tie, comp, lo, hi, compD,
+                                                                   compE, ties);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hook_contract(int32_t* comp, int64_t n, const unsigned long long* compD,
+                                 const unsigned long long* compE, int32_t* succ, int32_t* succ2,
+                                 int32_t* eu, int32_t* ev, double* ed, int32_t* ecount,
+                                 int32_t* changed, int32_t* nroots, cudaStream_t st) {
+    const unsigned g = blocks_for(n, 256);
+    hook_kernel<<<g, 256, 0, st>>>(comp, n, compE, succ);
+    resolve_emit_kernel<<<g, 256, 0, st>>>(comp, n, compE, compD, succ, succ2, eu, ev, ed, ecount);
+    // pointer jumping until every representative points at a root; a fixed
+    // number of passes (log2 n) avoids a host round trip per pass
+    int passes = 1;
+    while ((int64_t(1) << passes) < n) ++passes;
+    for (int p = 0; p < passes + 1; ++p) jump_kernel<<<g, 256, 0, st>>>(comp, n, succ2, changed);
+    cudaMemsetAsync(nroots, 0, sizeof(int32_t), st);
+    relabel_kernel<<<g, 256, 0, st>>>(comp, n, succ2, nroots);
+    return cudaGetLastError();
+}
+
+}  // namespace isoc

@@ -1,0 +1,595 @@
+// extern "C" entry points of libisoclust_b200.so (see include/isoclust_b200.h).
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/isoclust_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace isoc;
+
+static_assert(sizeof(FoldStack) == ISOC_FOLD_STACK_BYTES, "fold stack layout");
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(expr)                                                                              \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess) {                                                              \
+            cudaGetLastError();                                                               \
+            return fail(_e == cudaErrorMemoryAllocation ? ISOC_ENOMEM : ISOC_ECUDA,           \
+                        "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__,      \
+                        __LINE__);                                                            \
+        }                                                                                     \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+    return cudaMalloc(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T));
+}
+
+template <typename T>
+cudaError_t aalloc(T** p, size_t count, cudaStream_t st) {
+    return cudaMallocAsync(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), st);
+}
+
+__global__ void scale_kernel(double* v, int64_t m, double a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) v[i] = __dmul_rn(a, v[i]);
+}
+
+__global__ void iota_kernel(int32_t* v, int64_t m) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) v[i] = (int32_t)i;
+}
+
+__global__ void exp_kernel(const double* x, double* y, int64_t m) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) y[i] = isoc_exp(x[i]);
+}
+
+__global__ void root_flow_kernel(double* flow, int64_t root) { flow[root] = 0.0; }
+
+inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// Merge `count` stacks in place (ping-pong) until one remains; result in *out.
+cudaError_t fold_stacks(const FoldStack* in, int64_t count, FoldStack* out, int32_t* flags,
+                        cudaStream_t st) {
+    if (count == 1) return cudaMemcpyAsync(out, in, sizeof(FoldStack), cudaMemcpyDeviceToDevice, st);
+    FoldStack *a = nullptr, *b = nullptr;
+    const int64_t n1 = (count + 63) / 64;
+    cudaError_t e = aalloc(&a, n1, st);
+    if (e != cudaSuccess) return e;
+    e = aalloc(&b, n1, st);
+    if (e != cudaSuccess) return e;
+    launch_stack_merge(in, count, 64, a, flags, st);
+    int64_t cur = n1;
+    while (cur > 1) {
+        launch_stack_merge(a, cur, 64, b, flags, st);
+        cur = (cur + 63) / 64;
+        FoldStack* t = a; a = b; b = t;
+    }
+    cudaMemcpyAsync(out, a, sizeof(FoldStack), cudaMemcpyDeviceToDevice, st);
+    cudaFreeAsync(a, st);
+    cudaFreeAsync(b, st);
+    return cudaGetLastError();
+}
+}  // namespace
+
+extern "C" {
+
+int isoc_version(void) { return 1; }
+
+const char* isoc_last_error(void) { return g_err.c_str(); }
+
+int isoc_exp_dev(const double* x, double* y, int64_t m, void* stream) {
+    if (m <= 0) return ISOC_OK;
+    exp_kernel<<<blocks(m, 256), 256, 0, (cudaStream_t)stream>>>(x, y, m);
+    CK(cudaGetLastError());
+    return ISOC_OK;
+}
+
+// ------------------------------------------------------------------ sigma
+int isoc_sigma_partial(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi, double alpha,
+                       void* stack_dev, int32_t* nn_j, double* nn_d, int8_t* nn_tie, double* p_dev,
+                       void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1 (n=%lld, d=%d)", (long long)n, d);
+    if (lo < 0 || hi > n || lo >= hi) return fail(ISOC_EINVAL, "bad row range [%lld, %lld)", (long long)lo, (long long)hi);
+    if (n > (int64_t)INT32_MAX) return fail(ISOC_EINVAL, "n too large");
+    const int64_t rows = hi - lo;
+    const int want_p = alpha > 0.0;
+    double* row_vals = nullptr;
+    int32_t *row_deps = nullptr, *row_cnt = nullptr, *flags = nullptr, *sdep = nullptr;
+    double* sval = nullptr;
+    int8_t* sown = nullptr;
+    FoldStack* groups = nullptr;
+    CK(aalloc(&row_vals, sigma_rowstack_entries(rows), st));
+    CK(aalloc(&row_deps, sigma_rowstack_entries(rows), st));
+    CK(aalloc(&row_cnt, rows, st));
+    CK(aalloc(&flags, 1, st));
+    CK(aalloc(&sval, rows, st));
+    CK(aalloc(&sdep, rows, st));
+    CK(aalloc(&sown, rows, st));
+    const int64_t ng = (rows + 63) / 64;
+    CK(aalloc(&groups, ng, st));
+    CK(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    CK(cudaMemsetAsync(sown, 0, rows, st));
+    CK(launch_sigma_pass(X, n, d, lo, hi, want_p, row_vals, row_deps, row_cnt, flags, nn_j, nn_d,
+                         nn_tie, want_p ? p_dev : nullptr, st));
+    const int64_t b_hi = hi < n ? hi + 1 : n;  // boundaries lo+1 .. min(hi, n-1)
+    CK(launch_sigma_straddle(X, n, d, lo + 1, b_hi, sval, sdep, sown, st));
+    CK(launch_sigma_merge_rows(n, lo, hi, 64, row_vals, row_deps, row_cnt, sval, sdep, sown, groups,
+                               flags, st));
+    CK(fold_stacks(groups, ng, reinterpret_cast<FoldStack*>(stack_dev), flags, st));
+    if (want_p) {
+        scale_kernel<<<blocks(rows, 256), 256, 0, st>>>(p_dev, rows, alpha);
+        CK(cudaGetLastError());
+    } else if (p_dev) {
+        CK(cudaMemsetAsync(p_dev, 0, (size_t)rows * sizeof(double), st));
+    }
+    int32_t hflags = 0;
+    CK(cudaMemcpyAsync(&hflags, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(row_vals, st); cudaFreeAsync(row_deps, st); cudaFreeAsync(row_cnt, st);
+    cudaFreeAsync(sval, st); cudaFreeAsync(sdep, st); cudaFreeAsync(sown, st);
+    cudaFreeAsync(groups, st); cudaFreeAsync(flags, st);
+    CK(cudaStreamSynchronize(st));
+    if (hflags) return fail(ISOC_ECUDA, "pairwise fold stack overflow (flags=%d)", hflags);
+    return ISOC_OK;
+}
+
+int isoc_sigma_finish(const void* stacks_dev, int64_t nseg, double* total_host, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (nseg < 1) return fail(ISOC_EINVAL, "no fold stacks");
+    FoldStack* out = nullptr;
+    int32_t* flags = nullptr;
+    CK(aalloc(&out, 1, st));
+    CK(aalloc(&flags, 1, st));
+    CK(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    CK(fold_stacks(reinterpret_cast<const FoldStack*>(stacks_dev), nseg, out, flags, st));
+    FoldStack h;
+    CK(cudaMemcpyAsync(&h, out, sizeof(FoldStack), cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(out, st);
+    cudaFreeAsync(flags, st);
+    CK(cudaStreamSynchronize(st));
+    if (h.count != 1 || h.depth[0] != 0 || h.overflow)
+        return fail(ISOC_EINVAL, "fold stacks do not close to one root (count=%d depth=%d)", h.count,
+                    h.count > 0 ? h.depth[0] : -1);
+    *total_host = 0.0 + h.value[0];
+    return ISOC_OK;
+}
+
+// ------------------------------------------------------------------ omega
+int isoc_omega(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi, double sigma,
+               double* omega, void* stream) {
+    if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
+    if (!(sigma > 0.0)) return fail(ISOC_EINVAL, "sigma must be > 0, got %g", sigma);
+    if (lo < 0 || hi > n || lo >= hi) return fail(ISOC_EINVAL, "bad row range");
+    CK(launch_omega_pass(X, n, d, lo, hi, sigma, omega, (cudaStream_t)stream));
+    return ISOC_OK;
+}
+
+// -------------------------------------------------------------------- MST
+struct isoc_mst {
+    const double* X;
+    int64_t n, lo, hi, rows;
+    int32_t d, dp;
+    cudaStream_t st;
+    float cd;
+    float *Y, *ny, *rad;
+    double* centre;
+    uint32_t* rmax;
+    int32_t* comp;
+    float *a1, *a2;
+    int32_t* j1;
+    uint32_t* compB;
+    double* cand_d;
+    int32_t* cand_j;
+    int8_t *cand_state, *cand_tie;
+    int32_t *rescan_list, *counters;  // counters: rescan, ties, ecount, changed, nroots
+    int32_t *succ, *succ2;
+    int32_t *eu, *ev;
+    double* ed;
+};
+
+static void mst_free(isoc_mst* h) {
+    if (!h) return;
+    void* ptrs[] = {h->Y, h->ny, h->rad, h->centre, h->rmax, h->comp, h->a1, h->a2, h->j1,
+                    h->compB, h->cand_d, h->cand_j, h->cand_state, h->cand_tie, h->rescan_list,
+                    h->counters, h->succ, h->succ2, h->eu, h->ev, h->ed};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    delete h;
+}
+
+int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi, void* stream,
+                    isoc_mst** out) {
+    *out = nullptr;
+    if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
+    if (lo < 0 || hi > n || lo >= hi) return fail(ISOC_EINVAL, "bad row range");
+    if (n > (int64_t)INT32_MAX) return fail(ISOC_EINVAL, "n too large");
+    isoc_mst* h = new isoc_mst();
+    memset(h, 0, sizeof(*h));
+    h->X = X; h->n = n; h->d = d; h->lo = lo; h->hi = hi; h->rows = hi - lo;
+    h->dp = (d + 7) / 8 * 8;
+    h->st = (cudaStream_t)stream;
+    // rigorous FP32 Gram error coefficient, inflated ("filter bound")
+    h->cd = (float)((((double)d + 9.0) * 0x1p-24 + 0x1p-30) * 1.0625);
+#define MCK(expr)                                              \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) {                               \
+            mst_free(h);                                       \
+            cudaGetLastError();                                \
+            return fail(_e == cudaErrorMemoryAllocation ? ISOC_ENOMEM : ISOC_ECUDA, \
+                        "%s: %s", #expr, cudaGetErrorString(_e)); \
+        }                                                      \
+    } while (0)
+    MCK(dalloc(&h->Y, (size_t)n * h->dp));
+    MCK(dalloc(&h->ny, n));
+    MCK(dalloc(&h->rad, n));
+    MCK(dalloc(&h->centre, d));
+    MCK(dalloc(&h->rmax, 1));
+    MCK(dalloc(&h->comp, n));
+    MCK(dalloc(&h->a1, h->rows));
+    MCK(dalloc(&h->a2, h->rows));
+    MCK(dalloc(&h->j1, h->rows));
+    MCK(dalloc(&h->compB, n));
+    MCK(dalloc(&h->cand_d, h->rows));
+    MCK(dalloc(&h->cand_j, h->rows));
+    MCK(dalloc(&h->cand_state, h->rows));
+    MCK(dalloc(&h->cand_tie, h->rows));
+    MCK(dalloc(&h->rescan_list, h->rows));
+    MCK(dalloc(&h->counters, 8));
+    MCK(dalloc(&h->succ, n));
+    MCK(dalloc(&h->succ2, n));
+    MCK(dalloc(&h->eu, n));
+    MCK(dalloc(&h->ev, n));
+    MCK(dalloc(&h->ed, n));
+    MCK(cudaMemsetAsync(h->counters, 0, 8 * sizeof(int32_t), h->st));
+    iota_kernel<<<blocks(n, 256), 256, 0, h->st>>>(h->comp, n);
+    MCK(cudaGetLastError());
+    MCK(launch_prep_fp32(X, n, d, h->dp, h->centre, h->Y, h->ny, h->rad, h->rmax, h->st));
+#undef MCK
+    *out = h;
+    return ISOC_OK;
+}
+
+int isoc_mst_round_local(isoc_mst* h, int use_nn, const int32_t* nn_j, const double* nn_d,
+                         const int8_t* nn_tie, uint64_t* comp_min) {
+    cudaStream_t st = h->st;
+    if (use_nn) {
+        CK(launch_nn_candidates(nn_j, nn_d, nn_tie, h->rows, h->cand_d, h->cand_j, h->cand_state,
+                                h->cand_tie, st));
+    } else {
+        CK(launch_boruvka_filter(h->Y, h->ny, h->comp, h->n, h->dp, h->lo, h->hi, h->a1, h->j1, h->a2,
+                                 st));
+        CK(launch_boruvka_select(h->X, h->n, h->d, h->a1, h->j1, h->a2, h->rad, h->rmax, h->cd, h->comp,
+                                 h->lo, h->hi, h->compB, h->cand_d, h->cand_j, h->cand_state,
+                                 h->cand_tie, h->rescan_list, h->counters + 0, st));
+    }
+    CK(launch_comp_exact_min(h->cand_d, h->cand_state, h->comp, h->n, h->lo, h->hi,
+                             reinterpret_cast<unsigned long long*>(comp_min), st));
+    return ISOC_OK;
+}
+
+int isoc_mst_round_edges(isoc_mst* h, const uint64_t* comp_min, uint64_t* comp_edge) {
+    CK(launch_comp_edge(h->cand_d, h->cand_j, h->cand_state, h->comp, h->n, h->lo, h->hi,
+                        reinterpret_cast<const unsigned long long*>(comp_min),
+                        reinterpret_cast<unsigned long long*>(comp_edge), h->st));
+    return ISOC_OK;
+}
+
+int isoc_mst_round_finish(isoc_mst* h, const uint64_t* comp_min, const uint64_t* comp_edge,
+                          int64_t* components, int64_t* ties, int64_t* rescans) {
+    cudaStream_t st = h->st;
+    const auto* cm = reinterpret_cast<const unsigned long long*>(comp_min);
+    const auto* ce = reinterpret_cast<const unsigned long long*>(comp_edge);
+    CK(launch_comp_ties(h->cand_d, h->cand_j, h->cand_state, h->cand_tie, h->comp, h->lo, h->hi, cm,
+                        ce, h->counters + 1, st));
+    CK(launch_hook_contract(h->comp, h->n, cm, ce, h->succ, h->succ2, h->eu, h->ev, h->ed,
+                            h->counters + 2, h->counters + 3, h->counters + 4, st));
+    int32_t c[8];
+    CK(cudaMemcpyAsync(c, h->counters, sizeof c, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (components) *components = c[4];
+    if (ties) *ties = c[1];
+    if (rescans) *rescans = c[0];
+    if (c[2] > h->n - 1) return fail(ISOC_ECUDA, "MST edge overflow (%d edges)", c[2]);
+    return ISOC_OK;
+}
+
+int isoc_mst_edges(isoc_mst* h, int32_t* u, int32_t* v, double* w) {
+    int32_t cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, h->counters + 2, sizeof cnt, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (cnt != h->n - 1) return fail(ISOC_ECUDA, "MST has %d edges, expected %lld", cnt, (long long)(h->n - 1));
+    if (u) CK(cudaMemcpyAsync(u, h->eu, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st));
+    if (v) CK(cudaMemcpyAsync(v, h->ev, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st));
+    if (w) CK(cudaMemcpyAsync(w, h->ed, (size_t)cnt * 8, cudaMemcpyDeviceToDevice, h->st));
+    return ISOC_OK;
+}
+
+void isoc_mst_destroy(isoc_mst* h) {
+    if (h) cudaStreamSynchronize(h->st);
+    mst_free(h);
+}
+
+// ------------------------------------------------------------------- tree
+struct isoc_tree {
+    int64_t n, root, levels, max_width;
+    cudaStream_t st;
+    std::vector<int64_t> level_off_h;
+    int32_t *bfs, *pos_of, *parent_v, *depth_v, *child_id_v, *pos_parent, *child_lo, *child_cnt;
+    double *parent_d, *flow_v;
+    int64_t* level_off;
+    double *omega_v, *p_v, *f_pos, *om_pos, *p_pos;
+    double *om_w, *p_w;
+    int8_t* code[2];
+    double* spars[2];
+    int64_t spars_cap[2];
+    int32_t *excl, *scratch;
+    int64_t* j_out;
+};
+
+static void tree_free(isoc_tree* t) {
+    if (!t) return;
+    void* ptrs[] = {t->bfs, t->pos_of, t->parent_v, t->depth_v, t->child_id_v, t->pos_parent,
+                    t->child_lo, t->child_cnt, t->parent_d, t->flow_v, t->level_off, t->omega_v,
+                    t->p_v, t->f_pos, t->om_pos, t->p_pos, t->om_w, t->p_w, t->code[0], t->code[1],
+                    t->spars[0], t->spars[1], t->excl, t->scratch, t->j_out};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    delete t;
+}
+
+static int tree_alloc(isoc_tree* t, int64_t n) {
+    CK(dalloc(&t->bfs, n));
+    CK(dalloc(&t->pos_of, n));
+    CK(dalloc(&t->parent_v, n));
+    CK(dalloc(&t->depth_v, n));
+    CK(dalloc(&t->child_id_v, n));
+    CK(dalloc(&t->pos_parent, n));
+    CK(dalloc(&t->child_lo, n));
+    CK(dalloc(&t->child_cnt, n));
+    CK(dalloc(&t->parent_d, n));
+    CK(dalloc(&t->flow_v, n));
+    CK(dalloc(&t->level_off, n + 2));
+    CK(dalloc(&t->scratch, n + 4096));
+    CK(dalloc(&t->j_out, 4));
+    return ISOC_OK;
+}
+
+static int tree_finish_layout(isoc_tree* t, int64_t levels_dev_value) {
+    if (levels_dev_value <= 0) return fail(ISOC_EINVAL, "parent array does not describe one connected tree");
+    t->levels = levels_dev_value;
+    t->level_off_h.resize(t->levels + 1);
+    CK(cudaMemcpyAsync(t->level_off_h.data(), t->level_off, (t->levels + 1) * sizeof(int64_t),
+                       cudaMemcpyDeviceToHost, t->st));
+    CK(cudaStreamSynchronize(t->st));
+    if (t->level_off_h[t->levels] != t->n)
+        return fail(ISOC_EINVAL, "parent array does not describe one connected tree");
+    t->max_width = 0;
+    for (int64_t l = 0; l < t->levels; ++l)
+        t->max_width = std::max(t->max_width, t->level_off_h[l + 1] - t->level_off_h[l]);
+    return ISOC_OK;
+}
+
+int isoc_tree_from_edges(const int32_t* u, const int32_t* v, const double* w, int64_t n, int64_t root,
+                         double sigma, void* stream, isoc_tree** out) {
+    *out = nullptr;
+    if (n < 2) return fail(ISOC_EINVAL, "need at least 2 vertices");
+    if (root < 0 || root >= n) return fail(ISOC_EINVAL, "root must be in [0, %lld), got %lld", (long long)n, (long long)root);
+    if (!(sigma > 0.0)) return fail(ISOC_EINVAL, "sigma must be > 0, got %g", sigma);
+    isoc_tree* t = new isoc_tree();
+    t->n = n; t->root = root; t->st = (cudaStream_t)stream;
+    int rc = tree_alloc(t, n);
+    if (rc) { tree_free(t); return rc; }
+    int32_t *off = nullptr, *adj = nullptr, *work = nullptr;
+    double* adjd = nullptr;
+    int64_t* lv = nullptr;
+    cudaStream_t st = t->st;
+#define TCK(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { cudaGetLastError(); tree_free(t); \
+    return fail(_e == cudaErrorMemoryAllocation ? ISOC_ENOMEM : ISOC_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e)); } } while (0)
+    TCK(aalloc(&off, n + 1, st));
+    TCK(aalloc(&adj, 2 * n, st));
+    TCK(aalloc(&adjd, 2 * n, st));
+    TCK(aalloc(&work, n + 2, st));
+    TCK(aalloc(&lv, 1, st));
+    TCK(launch_build_adjacency(u, v, w, n, off, adj, adjd, work, st));
+    TCK(launch_bfs(n, root, 1, off, adj, adjd, t->bfs, t->pos_of, t->parent_v, t->depth_v,
+                   t->child_id_v, t->parent_d, t->pos_parent, t->child_lo, t->child_cnt, t->level_off,
+                   t->scratch, lv, st));
+    TCK(launch_flows(t->parent_d, t->parent_v, n, sigma, t->flow_v, st));
+    int64_t levels = 0;
+    TCK(cudaMemcpyAsync(&levels, lv, sizeof levels, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(off, st); cudaFreeAsync(adj, st); cudaFreeAsync(adjd, st);
+    cudaFreeAsync(work, st); cudaFreeAsync(lv, st);
+    TCK(cudaStreamSynchronize(st));
+    rc = tree_finish_layout(t, levels);
+    if (rc) { tree_free(t); return rc; }
+    *out = t;
+    return ISOC_OK;
+}
+
+int isoc_tree_from_parent(const int64_t* parent, const double* flow, const int64_t* child_id,
+                          int64_t n, int64_t root, void* stream, isoc_tree** out) {
+    *out = nullptr;
+    if (n < 1) return fail(ISOC_EINVAL, "empty parent array");
+    if (n > (int64_t)INT32_MAX - 1) return fail(ISOC_EINVAL, "n too large");
+    if (root < 0 || root >= n) return fail(ISOC_EINVAL, "root does not match the parent array's sentinel");
+    isoc_tree* t = new isoc_tree();
+    t->n = n; t->root = root; t->st = (cudaStream_t)stream;
+    int rc = tree_alloc(t, n);
+    if (rc) { tree_free(t); return rc; }
+    cudaStream_t st = t->st;
+    int32_t *off = nullptr, *adj = nullptr, *flags = nullptr;
+    int64_t* lv = nullptr;
+    TCK(aalloc(&off, n + 1, st));
+    TCK(aalloc(&adj, n, st));
+    TCK(aalloc(&flags, 2, st));
+    TCK(aalloc(&lv, 1, st));
+    TCK(cudaMemsetAsync(flags, 0, 2 * sizeof(int32_t), st));
+    TCK(launch_children_from_parent(parent, child_id, n, root, off, adj, t->child_id_v, flags,
+                                    flags + 1, st));
+    int32_t hf[2] = {0, 0};
+    TCK(cudaMemcpyAsync(hf, flags, 8, cudaMemcpyDeviceToHost, st));
+    const int32_t hflags = hf[0], nroots = hf[1];
+    TCK(cudaStreamSynchronize(st));
+    if (hflags & 2) { tree_free(t); return fail(ISOC_EINVAL, "parent indices out of range"); }
+    if (nroots != 1 || (hflags & 1)) {
+        tree_free(t);
+        return fail(ISOC_EINVAL, "expected exactly one root sentinel matching root, found %d", nroots);
+    }
+    TCK(launch_bfs(n, root, 0, off, adj, nullptr, t->bfs, t->pos_of, t->parent_v, t->depth_v,
+                   t->child_id_v, t->parent_d, t->pos_parent, t->child_lo, t->child_cnt, t->level_off,
+                   t->scratch, lv, st));
+    TCK(cudaMemcpyAsync(t->flow_v, flow, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+    root_flow_kernel<<<1, 1, 0, st>>>(t->flow_v, root);
+    int64_t levels = 0;
+    TCK(cudaMemcpyAsync(&levels, lv, sizeof levels, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(off, st); cudaFreeAsync(adj, st);
+    cudaFreeAsync(flags, st); cudaFreeAsync(lv, st);
+    TCK(cudaStreamSynchronize(st));
+    rc = tree_finish_layout(t, levels);
+    if (rc) { tree_free(t); return rc; }
+    *out = t;
+    return ISOC_OK;
+}
+
+int isoc_tree_export(isoc_tree* t, int64_t* parent, double* parent_flow, int64_t* depth,
+                     int64_t* child_id, int64_t* bfs_order, int64_t* max_depth, double* parent_dist) {
+    const int64_t n = t->n;
+    std::vector<int32_t> tmp(n);
+    auto pull32 = [&](const int32_t* src, int64_t* dst) -> int {
+        CK(cudaMemcpyAsync(tmp.data(), src, n * 4, cudaMemcpyDeviceToHost, t->st));
+        CK(cudaStreamSynchronize(t->st));
+        for (int64_t i = 0; i < n; ++i) dst[i] = tmp[i];
+        return ISOC_OK;
+    };
+    int rc;
+    if (parent && (rc = pull32(t->parent_v, parent))) return rc;
+    if (depth && (rc = pull32(t->depth_v, depth))) return rc;
+    if (child_id && (rc = pull32(t->child_id_v, child_id))) return rc;
+    if (bfs_order) {
+        CK(cudaMemcpyAsync(tmp.data(), t->bfs, n * 4, cudaMemcpyDeviceToHost, t->st));
+        CK(cudaStreamSynchronize(t->st));
+        for (int64_t i = 0; i < n; ++i) bfs_order[i] = tmp[n - 1 - i];
+    }
+    if (parent_flow) CK(cudaMemcpyAsync(parent_flow, t->flow_v, n * 8, cudaMemcpyDeviceToHost, t->st));
+    if (parent_dist) CK(cudaMemcpyAsync(parent_dist, t->parent_d, n * 8, cudaMemcpyDeviceToHost, t->st));
+    CK(cudaStreamSynchronize(t->st));
+    if (max_depth) *max_depth = t->levels - 1;
+    return ISOC_OK;
+}
+
+int isoc_tree_set_weights(isoc_tree* t, const double* omega, const double* p, double* extrema) {
+    const int64_t n = t->n;
+    cudaStream_t st = t->st;
+    if (!t->omega_v) {
+        CK(dalloc(&t->omega_v, n)); CK(dalloc(&t->p_v, n));
+        CK(dalloc(&t->f_pos, n)); CK(dalloc(&t->om_pos, n)); CK(dalloc(&t->p_pos, n));
+        CK(dalloc(&t->om_w, n)); CK(dalloc(&t->p_w, n));
+        CK(dalloc(&t->code[0], n)); CK(dalloc(&t->code[1], n));
+        CK(dalloc(&t->excl, n));
+    }
+    CK(cudaMemcpyAsync(t->omega_v, omega, n * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(t->p_v, p, n * 8, cudaMemcpyDeviceToDevice, st));
+    CK(launch_gather_pos(t->bfs, n, t->flow_v, t->omega_v, t->p_v, t->f_pos, t->om_pos, t->p_pos, st));
+    if (extrema) {
+        double* out6 = nullptr;
+        double* tmp = nullptr;
+        unsigned long long* key = nullptr;
+        int64_t P = 1;
+        while (P < n) P <<= 1;
+        CK(aalloc(&out6, 6, st));
+        CK(aalloc(&tmp, 2 * (P / 2048 + 2), st));
+        CK(aalloc(&key, 3, st));
+        CK(launch_extrema(t->flow_v, t->root, t->omega_v, t->p_v, n, out6, tmp, key, st));
+        CK(cudaMemcpyAsync(extrema, out6, 6 * 8, cudaMemcpyDeviceToHost, st));
+        cudaFreeAsync(out6, st); cudaFreeAsync(tmp, st); cudaFreeAsync(key, st);
+        CK(cudaStreamSynchronize(st));
+    }
+    return ISOC_OK;
+}
+
+int isoc_decide(isoc_tree* t, double N, int64_t k, int32_t slot, int64_t* j_host) {
+    if (!t->omega_v) return fail(ISOC_EINVAL, "weights not attached");
+    if (k < 1) return fail(ISOC_EINVAL, "k must be >= 1, got %lld", (long long)k);
+    if (!std::isfinite(N)) return fail(ISOC_EINVAL, "threshold must be finite, got %g", N);
+    if (slot < 0 || slot > 1) return fail(ISOC_EINVAL, "slot must be 0 or 1");
+    cudaStream_t st = t->st;
+    if (t->spars_cap[slot] < k) {
+        if (t->spars[slot]) cudaFree(t->spars[slot]);
+        t->spars[slot] = nullptr;
+        CK(dalloc(&t->spars[slot], k));
+        t->spars_cap[slot] = k;
+    }
+    CK(launch_decide(t->n, t->levels, t->level_off, t->max_width, t->f_pos, t->om_pos, t->p_pos,
+                     t->child_lo, t->child_cnt, N, k, t->om_w, t->p_w, t->code[slot], t->excl,
+                     t->spars[slot], t->scratch, t->j_out, st));
+    CK(cudaMemcpyAsync(j_host, t->j_out, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return ISOC_OK;
+}
+
+int isoc_witness(isoc_tree* t, int32_t slot, int64_t k, int64_t* labels, int8_t* cut, int64_t* eta,
+                 double* sparsities, double* miso) {
+    const int64_t n = t->n;
+    cudaStream_t st = t->st;
+    if (slot < 0 || slot > 1 || !t->code[slot]) return fail(ISOC_EINVAL, "no witness in slot %d", slot);
+    int8_t* cut_v = nullptr;
+    int64_t *eta_v = nullptr, *lab_v = nullptr;
+    int32_t *lab32 = nullptr, *work = nullptr;
+    double *sums = nullptr, *miso_d = nullptr;
+    void* cwork = nullptr;
+    const size_t cbytes = cost_work_bytes(n, k);
+    CK(aalloc(&cut_v, n, st));
+    CK(aalloc(&eta_v, n, st));
+    CK(aalloc(&lab_v, n, st));
+    CK(aalloc(&lab32, n, st));
+    CK(aalloc(&work, 4 * n, st));
+    CK(aalloc(&sums, 3 * k, st));
+    CK(aalloc(&miso_d, 1, st));
+    CK(cudaMallocAsync(&cwork, cbytes, st));
+    CK(launch_labels(t->code[slot], t->pos_parent, t->bfs, n, t->levels, cut_v, eta_v, lab_v, lab32,
+                     work, st));
+    CK(launch_cost(lab32, t->parent_v, t->flow_v, t->omega_v, t->p_v, n, k, cwork, cbytes, sums,
+                   miso_d, st));
+    if (labels) CK(cudaMemcpyAsync(labels, lab_v, n * 8, cudaMemcpyDeviceToHost, st));
+    if (cut) CK(cudaMemcpyAsync(cut, cut_v, n, cudaMemcpyDeviceToHost, st));
+    if (eta) CK(cudaMemcpyAsync(eta, eta_v, n * 8, cudaMemcpyDeviceToHost, st));
+    if (sparsities && t->spars[slot])
+        CK(cudaMemcpyAsync(sparsities, t->spars[slot], k * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(miso, miso_d, 8, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(cut_v, st); cudaFreeAsync(eta_v, st); cudaFreeAsync(lab_v, st);
+    cudaFreeAsync(lab32, st); cudaFreeAsync(work, st); cudaFreeAsync(sums, st);
+    cudaFreeAsync(miso_d, st); cudaFreeAsync(cwork, st);
+    CK(cudaStreamSynchronize(st));
+    return ISOC_OK;
+}
+
+void isoc_tree_destroy(isoc_tree* t) {
+    if (t) cudaStreamSynchronize(t->st);
+    tree_free(t);
+}
+
+}  // extern "C"

@@ -1,0 +1,462 @@
+// Tree phase on the device: the level-synchronous decision sweep, witness
+// labels and the exact subpartition cost.
+//
+//  decide_kernel restates par_decide (/root/reference/pkg/src/isoclust/
+//  parengine.py:116-209), itself field-for-field equal to decide
+//  (isoperim.py:82-144).  Vertices live in BFS-position space, so a level is
+//  a contiguous position range and the canonical (reverse-BFS) order inside
+//  a level is descending position.  Per level:
+//    A  branch conditions on frozen state, cut counts per CTA chunk
+//    B  exclusive cut prefix in canonical order; a vertex is committed iff
+//       fewer than (k - j) cuts precede it (stop at the k-th cut); committed
+//       cuts record their sparsity at slot j + prefix (cut order)
+//    C  one thread per parent folds its committed children in descending
+//       child rank (the reference's serial same-parent commit order)
+//  One cooperative launch covers all levels (software grid barrier).
+//
+//  labels: extract_labels (isoperim.py:164-181) + _resolve_groups (:147-161)
+//  cost:   subpartition_cost (isoperim.py:184-219) with numpy's pairwise
+//          np.sum on the stably compacted per-cluster arrays.
+#include <cstdint>
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace isoc {
+
+static inline unsigned nb(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+struct DecideArgs {
+    int64_t n;
+    int64_t levels;
+    const int64_t* level_off;
+    const double* f_pos;
+    const double* om0;
+    const double* p0;
+    const int32_t* child_lo;
+    const int32_t* child_cnt;
+    double thr;
+    int64_t k;
+    double* om;
+    double* p;
+    int8_t* code;       // 0 uncommitted, 1 cut, 2 join, 3 discard
+    int32_t* excl;      // per-position chunk-local exclusive cut count
+    double* spars;      // k
+    int32_t* chunk_cnt; // gridDim.x
+    int64_t* j_out;
+    unsigned int* bar;
+};
+
+__global__ void __launch_bounds__(512) decide_kernel(DecideArgs A) {
+    __shared__ int32_t warp_tot[16];
+    __shared__ int64_t s_off, s_tot;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int G = gridDim.x, b = blockIdx.x;
+    const int64_t n = A.n;
+    // working copies (inputs are never mutated)
+    for (int64_t q = (int64_t)b * blockDim.x + tid; q < n; q += (int64_t)G * blockDim.x) {
+        A.om[q] = A.om0[q];
+        A.p[q] = A.p0[q];
+        A.code[q] = 0;
+    }
+    grid_barrier(A.bar);
+    int64_t j = 0;
+    const double thr = A.thr;
+    for (int64_t lv = A.levels - 1; lv >= 0; --lv) {
+        const int64_t lo = A.level_off[lv], hi = A.level_off[lv + 1];
+        const int64_t W = hi - lo;
+        // canonical index c in [0, W) <-> position hi-1-c
+        const int64_t cb = W * b / G, ce = W * (b + 1) / G;
+        int64_t carry = 0;
+        for (int64_t base = cb; base < ce; base += blockDim.x) {
+            const int64_t c = base + tid;
+            int32_t is_cut = 0;
+            int8_t cond = 0;
+            if (c < ce) {
+                const int64_t pos = hi - 1 - c;
+                const double f = A.f_pos[pos], pw = A.p[pos], ow = A.om[pos];
+                const double rhs = __dmul_rn(thr, ow);
+                if (__dadd_rn(f, pw) <= rhs) cond = 1;
+                else if (__dsub_rn(pw, f) < rhs) cond = 2;
+                else cond = 3;
+                is_cut = cond == 1;
+                A.code[pos] = cond;  // provisional; cleared in B if not committed
+            }
+            int32_t x = is_cut;
+            for (int o = 1; o < 32; o <<= 1) {
+                int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) warp_tot[wid] = x;
+            __syncthreads();
+            if (wid == 0) {
+                int32_t t = lane < nw ? warp_tot[lane] : 0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                    if (lane >= o) t += y;
+                }
+                if (lane < nw) warp_tot[lane] = t;
+            }
+            __syncthreads();
+            const int32_t wpre = wid > 0 ? warp_tot[wid - 1] : 0;
+            if (c < ce) A.excl[hi - 1 - c] = (int32_t)(carry + wpre + x - is_cut);
+            carry += warp_tot[nw - 1];
+            __syncthreads();
+        }
+        if (tid == 0) A.chunk_cnt[b] = (int32_t)carry;
+        grid_barrier(A.bar);
+        if (tid == 0) {
+            int64_t pre = 0, tot = 0;
+            for (int q = 0; q < G; ++q) {
+                const int64_t s = A.chunk_cnt[q];
+                if (q < b) pre += s;
+                tot += s;
+            }
+            s_off = pre;
+            s_tot = tot;
+        }
+        __syncthreads();
+        const int64_t need = A.k - j;
+        const int64_t off = s_off, tot = s_tot;
+        for (int64_t c = cb + tid; c < ce; c += blockDim.x) {
+            const int64_t pos = hi - 1 - c;
+            const int64_t e = off + A.excl[pos];
+            if (e < need) {
+                if (A.code[pos] == 1)
+                    A.spars[j + e] = __ddiv_rn(__dadd_rn(A.f_pos[pos], A.p[pos]), A.om[pos]);
+            } else {
+                A.code[pos] = 0;
+            }
+        }
+        grid_barrier(A.bar);
+        if (lv > 0) {
+            const int64_t plo = A.level_off[lv - 1], phi = lo;
+            const int64_t PW = phi - plo;
+            for (int64_t u = plo + (PW * b) / G + tid; u < plo + (PW * (b + 1)) / G; u += blockDim.x) {
+                const int32_t clo = A.child_lo[u], cnt = A.child_cnt[u];
+                double pu = A.p[u], ou = A.om[u];
+                bool touched = false;
+                for (int32_t q = clo + cnt - 1; q >= clo; --q) {
+                    const int8_t cd = A.code[q];
+                    if (cd == 1 || cd == 3) {
+                        pu = __dadd_rn(pu, A.f_pos[q]);
+                        touched = true;
+                    } else if (cd == 2) {
+                        ou = __dadd_rn(ou, A.om[q]);
+                        pu = __dadd_rn(pu, A.p[q]);
+                        touched = true;
+                    }
+                }
+                if (touched) {
+                    A.p[u] = pu;
+                    A.om[u] = ou;
+                }
+            }
+        }
+        j += (tot < need) ? tot : need;
+        grid_barrier(A.bar);
+        if (j >= A.k) break;
+    }
+    if (b == 0 && tid == 0) *A.j_out = j;
+}
+
+int decide_grid_size(int64_t max_width) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decide_kernel, 512, 0);
+    int64_t want = (max_width + 8191) / 8192;
+    int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    if (want < 1) want = 1;
+    return (int)(want < cap ? want : cap);
+}
+
+cudaError_t launch_decide(int64_t n, int64_t levels, const int64_t* level_off, int64_t max_width,
+                          const double* f_pos, const double* om0, const double* p0,
+                          const int32_t* child_lo, const int32_t* child_cnt, double thr, int64_t k,
+                          double* om, double* p, int8_t* code, int32_t* excl, double* spars,
+                          int32_t* scratch, int64_t* j_out, cudaStream_t st) {
+    const int G = decide_grid_size(max_width);
+    DecideArgs A;
+    A.n = n; A.levels = levels; A.level_off = level_off; A.f_pos = f_pos; A.om0 = om0; A.p0 = p0;
+    A.child_lo = child_lo; A.child_cnt = child_cnt; A.thr = thr; A.k = k; A.om = om; A.p = p;
+    A.code = code; A.excl = excl; A.spars = spars; A.chunk_cnt = scratch; A.j_out = j_out;
+    A.bar = reinterpret_cast<unsigned int*>(scratch + 1024);
+    cudaMemsetAsync(A.bar, 0, 2 * sizeof(unsigned int), st);
+    void* args[] = {&A};
+    return cudaLaunchCooperativeKernel((void*)decide_kernel, dim3(G), dim3(512), args, 0, st);
+}
+
+// ----------------------------------------------------------------- labels
+__global__ void rep_init_kernel(const int8_t* __restrict__ code, const int32_t* __restrict__ pos_parent,
+                                int64_t n, int32_t* __restrict__ rep) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    rep[q] = code[q] == 2 ? pos_parent[q] : (int32_t)q;
+}
+
+__global__ void rep_jump_kernel(const int32_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    out[q] = in[in[q]];
+}
+
+__global__ void cut_vertex_kernel(const int8_t* __restrict__ code, const int32_t* __restrict__ bfs,
+                                  int64_t n, int8_t* __restrict__ cut_v, int32_t* __restrict__ cut_i) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int32_t v = bfs[q];
+    const int8_t c = code[q] == 1;
+    cut_v[v] = c;
+    cut_i[v] = c;
+}
+
+__global__ void labels_kernel(const int32_t* __restrict__ rep, const int8_t* __restrict__ code,
+                              const int32_t* __restrict__ bfs, const int32_t* __restrict__ scan,
+                              int64_t n, int64_t* __restrict__ eta, int64_t* __restrict__ labels,
+                              int32_t* __restrict__ lab32) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int32_t v = bfs[q];
+    const int32_t r = rep[q];
+    if (code[r] == 1) {
+        const int32_t rv = bfs[r];
+        eta[v] = rv;
+        labels[v] = 1 + scan[rv];
+        lab32[v] = 1 + scan[rv];
+    } else {
+        eta[v] = ISOC_NO_VERTEX;
+        labels[v] = 0;
+        lab32[v] = 0;
+    }
+}
+
+cudaError_t launch_labels(const int8_t* code, const int32_t* pos_parent, const int32_t* bfs,
+                          int64_t n, int64_t levels, int8_t* cut_v, int64_t* eta, int64_t* labels,
+                          int32_t* lab32, int32_t* work, cudaStream_t st) {
+    // work: rep[n], rep2[n], cut_i[n], scan[n]
+    int32_t* rep = work;
+    int32_t* rep2 = work + n;
+    int32_t* cut_i = work + 2 * n;
+    int32_t* scan = work + 3 * n;
+    rep_init_kernel<<<nb(n, 256), 256, 0, st>>>(code, pos_parent, n, rep);
+    int passes = 0;
+    while ((int64_t(1) << passes) < levels + 1) ++passes;
+    for (int i = 0; i < passes; ++i) {
+        rep_jump_kernel<<<nb(n, 256), 256, 0, st>>>(rep, n, rep2);
+        int32_t* t = rep; rep = rep2; rep2 = t;
+    }
+    cut_vertex_kernel<<<nb(n, 256), 256, 0, st>>>(code, bfs, n, cut_v, cut_i);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cut_i, scan, (int)n, st);
+    void* tmp = nullptr;
+    cudaError_t e = cudaMallocAsync(&tmp, tb, st);
+    if (e != cudaSuccess) return e;
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cut_i, scan, (int)n, st);
+    cudaFreeAsync(tmp, st);
+    labels_kernel<<<nb(n, 256), 256, 0, st>>>(rep, code, bfs, scan, n, eta, labels, lab32);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- cost
+// keys (cluster << 32 | index) for member and crossing-edge entries;
+// cluster k+1 marks "no entry".
+__global__ void cost_keys_kernel(const int32_t* __restrict__ lab, const int32_t* __restrict__ parent_v,
+                                 const double* __restrict__ flow, const double* __restrict__ omega,
+                                 const double* __restrict__ p, int64_t n, int64_t k,
+                                 unsigned long long* __restrict__ mkeys, int32_t* __restrict__ mvals,
+                                 unsigned long long* __restrict__ bkeys, double* __restrict__ bvals) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const uint64_t none = (uint64_t)(k + 1) << 32;
+    const int32_t lu = lab[u];
+    mkeys[u] = lu >= 1 ? (((uint64_t)lu << 32) | (uint64_t)u) : (none | (uint64_t)u);
+    mvals[u] = (int32_t)u;
+    const int32_t pu = parent_v[u];
+    uint64_t ka = none | (uint64_t)u, kb = none | (uint64_t)u;
+    if (pu >= 0) {
+        const int32_t lp = lab[pu];
+        if (lu != lp) {
+            if (lu >= 1) ka = ((uint64_t)lu << 32) | (uint64_t)u;
+            if (lp >= 1) kb = ((uint64_t)lp << 32) | (uint64_t)u;
+        }
+    }
+    bkeys[u] = ka;
+    bkeys[n + u] = kb;
+    const double f = pu >= 0 ? flow[u] : 0.0;
+    bvals[u] = f;
+    bvals[n + u] = f;
+}
+
+// first sorted index of each cluster c in [1, k+1]
+__global__ void segment_bounds_kernel(const unsigned long long* __restrict__ keys, int64_t m,
+                                      int64_t k, int64_t* __restrict__ seg) {
+    const int64_t c = 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > k + 1) return;
+    const unsigned long long target = (unsigned long long)c << 32;
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (keys[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    seg[c - 1] = lo;
+}
+
+// slot s of a segment's depth-T grid: the pairwise-recursion node reached by
+// the T path bits of s; a leaf met earlier is owned by the slot whose
+// remaining bits are zero, others are empty.
+template <typename Get>
+__device__ double slot_value(Get get, int64_t m, int T, int64_t s, bool& empty) {
+    int64_t start = 0, len = m;
+    for (int t = 0; t < T; ++t) {
+        if (len <= 128) {
+            const int64_t rest = s & ((int64_t(1) << (T - t)) - 1);
+            if (rest != 0) { empty = true; return 0.0; }
+            break;
+        }
+        const int64_t n2 = np_split(len);
+        if ((s >> (T - 1 - t)) & 1) { start += n2; len -= n2; } else { len = n2; }
+    }
+    empty = false;
+    if (len > 128) return np_pairwise_small([&](int64_t i) { return get(start + i); }, len);
+    return np_leaf_sum([&](int64_t i) { return get(start + i); }, len);
+}
+
+__host__ __device__ __forceinline__ int seg_depth(int64_t m) {
+    int T = 0;
+    while ((m >> T) > 64) ++T;
+    return T;
+}
+
+// sum over segments of 2 * 2^T: 2^T <= max(1, 2m/64) and the segment
+// lengths total at most 2n (boundary) + n + n (members twice)
+static inline int64_t cost_slot_bound(int64_t n, int64_t k) { return 2 * (4 * n / 32 + 3 * k) + 64; }
+
+// Per (cluster, quantity) segment: 0 = boundary flows, 1 = potentials,
+// 2 = masses.  slot_off holds each segment's scratch offset (2 * 2^T values
+// and flags, double-buffered) computed on the device from the bounds.
+__global__ void slot_offsets_kernel(const int64_t* __restrict__ bseg, const int64_t* __restrict__ mseg,
+                                    int64_t k, int64_t* __restrict__ slot_off) {
+    int64_t acc = 0;
+    for (int64_t q = 0; q < 3 * k; ++q) {
+        const int64_t c = q / 3;
+        const int64_t* seg = (q % 3) == 0 ? bseg : mseg;
+        const int64_t m = seg[c + 1] - seg[c];
+        slot_off[q] = acc;
+        acc += 2 * (int64_t(1) << seg_depth(m));
+    }
+    slot_off[3 * k] = acc;
+}
+
+// One CTA per segment: slot values, then a binary fold where an empty right
+// slot passes the left value through unchanged (the leaf above it IS the node).
+__global__ void segment_sum_kernel(const double* __restrict__ bvals_sorted,
+                                   const int32_t* __restrict__ mvals_sorted,
+                                   const double* __restrict__ omega, const double* __restrict__ p,
+                                   const int64_t* __restrict__ bseg, const int64_t* __restrict__ mseg,
+                                   const int64_t* __restrict__ slot_off, double* __restrict__ vals,
+                                   uint8_t* __restrict__ flags, double* __restrict__ sums) {
+    const int64_t c = blockIdx.x / 3;
+    const int what = blockIdx.x % 3;
+    const int64_t* seg = what == 0 ? bseg : mseg;
+    const int64_t a = seg[c], m = seg[c + 1] - seg[c];
+    if (m == 0) {
+        if (threadIdx.x == 0) sums[blockIdx.x] = 0.0;
+        return;
+    }
+    const int T = seg_depth(m);
+    const int64_t S = int64_t(1) << T;
+    double* v0 = vals + slot_off[blockIdx.x];
+    double* v1 = v0 + S;
+    uint8_t* e0 = flags + slot_off[blockIdx.x];
+    uint8_t* e1 = e0 + S;
+    auto get = [&](int64_t i) -> double {
+        if (what == 0) return bvals_sorted[a + i];
+        const int32_t v = mvals_sorted[a + i];
+        return what == 1 ? p[v] : omega[v];
+    };
+    for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {
+        bool e = false;
+        v0[s] = slot_value(get, m, T, s, e);
+        e0[s] = e;
+    }
+    __syncthreads();
+    for (int64_t w = S; w > 1; w >>= 1) {
+        for (int64_t i = threadIdx.x; i < w / 2; i += blockDim.x) {
+            const double l = v0[2 * i], r = v0[2 * i + 1];
+            v1[i] = e0[2 * i + 1] ? l : __dadd_rn(l, r);
+            e1[i] = e0[2 * i];
+        }
+        __syncthreads();
+        double* tv = v0; v0 = v1; v1 = tv;
+        uint8_t* te = e0; e0 = e1; e1 = te;
+    }
+    if (threadIdx.x == 0) sums[blockIdx.x] = __dadd_rn(0.0, v0[0]);
+}
+
+__global__ void miso_kernel(const double* __restrict__ sums, int64_t k, double* __restrict__ out) {
+    double worst = -INFINITY;
+    for (int64_t c = 0; c < k; ++c) {
+        const double s = __ddiv_rn(__dadd_rn(sums[3 * c + 0], sums[3 * c + 1]), sums[3 * c + 2]);
+        worst = fmax(worst, s);
+    }
+    *out = worst;
+}
+
+cudaError_t launch_cost(const int32_t* lab32, const int32_t* parent_v, const double* flow,
+                        const double* omega, const double* p, int64_t n, int64_t k,
+                        void* work, size_t work_bytes, double* sums, double* miso, cudaStream_t st) {
+    // work layout
+    char* w = reinterpret_cast<char*>(work);
+    auto take = [&](size_t bytes) { char* r = w; w += (bytes + 255) & ~size_t(255); return r; };
+    unsigned long long* mkeys = (unsigned long long*)take(8 * n);
+    unsigned long long* mkeys_s = (unsigned long long*)take(8 * n);
+    int32_t* mvals = (int32_t*)take(4 * n);
+    int32_t* mvals_s = (int32_t*)take(4 * n);
+    unsigned long long* bkeys = (unsigned long long*)take(16 * n);
+    unsigned long long* bkeys_s = (unsigned long long*)take(16 * n);
+    double* bvals = (double*)take(16 * n);
+    double* bvals_s = (double*)take(16 * n);
+    int64_t* mseg = (int64_t*)take(8 * (k + 2));
+    int64_t* bseg = (int64_t*)take(8 * (k + 2));
+    int64_t* slot_off = (int64_t*)take(8 * (3 * k + 1));
+    const int64_t slots = cost_slot_bound(n, k);
+    double* svals = (double*)take(8 * slots);
+    uint8_t* sflags = (uint8_t*)take(slots);
+    if ((size_t)(w - reinterpret_cast<char*>(work)) > work_bytes) return cudaErrorInvalidValue;
+
+    cost_keys_kernel<<<nb(n, 256), 256, 0, st>>>(lab32, parent_v, flow, omega, p, n, k, mkeys, mvals,
+                                                  bkeys, bvals);
+    int bits = 32;
+    while ((int64_t(1) << (bits - 32)) <= k + 1) ++bits;
+    size_t tb1 = 0, tb2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb1, mkeys, mkeys_s, mvals, mvals_s, (int)n, 0, bits, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, tb2, bkeys, bkeys_s, bvals, bvals_s, (int)(2 * n), 0, bits,
+                                    st);
+    void* tmp = nullptr;
+    cudaError_t e = cudaMallocAsync(&tmp, tb1 > tb2 ? tb1 : tb2, st);
+    if (e != cudaSuccess) return e;
+    cub::DeviceRadixSort::SortPairs(tmp, tb1, mkeys, mkeys_s, mvals, mvals_s, (int)n, 0, bits, st);
+    cub::DeviceRadixSort::SortPairs(tmp, tb2, bkeys, bkeys_s, bvals, bvals_s, (int)(2 * n), 0, bits, st);
+    cudaFreeAsync(tmp, st);
+    segment_bounds_kernel<<<nb(k + 1, 128), 128, 0, st>>>(mkeys_s, n, k, mseg);
+    segment_bounds_kernel<<<nb(k + 1, 128), 128, 0, st>>>(bkeys_s, 2 * n, k, bseg);
+    slot_offsets_kernel<<<1, 1, 0, st>>>(bseg, mseg, k, slot_off);
+    segment_sum_kernel<<<(unsigned)(3 * k), 256, 0, st>>>(bvals_s, mvals_s, omega, p, bseg, mseg,
+                                                          slot_off, svals, sflags, sums);
+    miso_kernel<<<1, 1, 0, st>>>(sums, k, miso);
+    return cudaGetLastError();
+}
+
+size_t cost_work_bytes(int64_t n, int64_t k) {
+    const int64_t slots = cost_slot_bound(n, k);
+    size_t b = 0;
+    auto add = [&](size_t bytes) { b += (bytes + 255) & ~size_t(255); };
+    add(8 * n); add(8 * n); add(4 * n); add(4 * n); add(16 * n); add(16 * n); add(16 * n); add(16 * n);
+    add(8 * (k + 2)); add(8 * (k + 2)); add(8 * (3 * k + 1)); add(8 * slots); add(slots);
+    return b;
+}
+
+}  // namespace isoc

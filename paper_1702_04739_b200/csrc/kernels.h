@@ -1,0 +1,92 @@
+// Internal launcher declarations (not part of the public C ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace isoc {
+struct FoldStack;
+
+// exact_passes.cu
+size_t sigma_rowstack_entries(int64_t rows);
+cudaError_t launch_sigma_pass(const double* X, int64_t n, int d, int64_t lo, int64_t hi, int want_p,
+                              double* row_vals, int32_t* row_deps, int32_t* row_cnt, int32_t* flags,
+                              int32_t* nn_j, double* nn_d, int8_t* nn_tie, double* pfold,
+                              cudaStream_t st);
+cudaError_t launch_sigma_straddle(const double* X, int64_t n, int d, int64_t b_lo, int64_t b_hi,
+                                  double* sval, int32_t* sdep, int8_t* sown, cudaStream_t st);
+cudaError_t launch_sigma_merge_rows(int64_t n, int64_t lo, int64_t hi, int G, const double* row_vals,
+                                    const int32_t* row_deps, const int32_t* row_cnt,
+                                    const double* sval, const int32_t* sdep, const int8_t* sown,
+                                    FoldStack* out, int32_t* flags, cudaStream_t st);
+cudaError_t launch_stack_merge(const FoldStack* in, int64_t nin, int G, FoldStack* out,
+                               int32_t* flags, cudaStream_t st);
+cudaError_t launch_omega_pass(const double* X, int64_t n, int d, int64_t lo, int64_t hi,
+                              double sigma, double* omega, cudaStream_t st);
+
+// boruvka.cu
+cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, double* centre, float* Y,
+                             float* ny, float* rad, uint32_t* rmax_bits, cudaStream_t st);
+cudaError_t launch_boruvka_filter(const float* Y, const float* ny, const int32_t* comp, int64_t n,
+                                  int dp, int64_t lo, int64_t hi, float* a1, int32_t* j1, float* a2,
+                                  cudaStream_t st);
+cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float* a1,
+                                  const int32_t* j1, const float* a2, const float* rad,
+                                  const uint32_t* rmax_bits, float cd, const int32_t* comp,
+                                  int64_t lo, int64_t hi, uint32_t* compB, double* cand_d,
+                                  int32_t* cand_j, int8_t* cand_state, int8_t* cand_tie,
+                                  int32_t* rescan_list, int32_t* rescan_count, cudaStream_t st);
+cudaError_t launch_nn_candidates(const int32_t* nn_j, const double* nn_d, const int8_t* nn_tie,
+                                 int64_t rows, double* cand_d, int32_t* cand_j, int8_t* cand_state,
+                                 int8_t* cand_tie, cudaStream_t st);
+cudaError_t launch_comp_exact_min(const double* cand_d, const int8_t* cand_state,
+                                  const int32_t* comp, int64_t n, int64_t lo, int64_t hi,
+                                  unsigned long long* compD, cudaStream_t st);
+cudaError_t launch_comp_edge(const double* cand_d, const int32_t* cand_j, const int8_t* cand_state,
+                             const int32_t* comp, int64_t n, int64_t lo, int64_t hi,
+                             const unsigned long long* compD, unsigned long long* compE,
+                             cudaStream_t st);
+cudaError_t launch_comp_ties(const double* cand_d, const int32_t* cand_j, const int8_t* cand_state,
+                             const int8_t* cand_tie, const int32_t* comp, int64_t lo, int64_t hi,
+                             const unsigned long long* compD, const unsigned long long* compE,
+                             int32_t* ties, cudaStream_t st);
+cudaError_t launch_hook_contract(int32_t* comp, int64_t n, const unsigned long long* compD,
+                                 const unsigned long long* compE, int32_t* succ, int32_t* succ2,
+                                 int32_t* eu, int32_t* ev, double* ed, int32_t* ecount,
+                                 int32_t* changed, int32_t* nroots, cudaStream_t st);
+
+// tree.cu
+cudaError_t launch_build_adjacency(const int32_t* eu, const int32_t* ev, const double* ed,
+                                   int64_t n, int32_t* off, int32_t* adj, double* adjd,
+                                   int32_t* work, cudaStream_t st);
+cudaError_t launch_children_from_parent(const int64_t* parent, const int64_t* child_id, int64_t n,
+                                        int64_t root, int32_t* off, int32_t* adj, int32_t* child_id_v,
+                                        int32_t* flags, int32_t* nroots, cudaStream_t st);
+cudaError_t launch_bfs(int64_t n, int64_t root, int undirected, const int32_t* off,
+                       const int32_t* adj, const double* adjd, int32_t* bfs, int32_t* pos_of,
+                       int32_t* parent_v, int32_t* depth_v, int32_t* child_id_v, double* parent_d,
+                       int32_t* pos_parent, int32_t* child_lo, int32_t* child_cnt,
+                       int64_t* level_off, int32_t* scratch, int64_t* out_levels, cudaStream_t st);
+cudaError_t launch_flows(const double* parent_d, const int32_t* parent_v, int64_t n, double sigma,
+                         double* flow, cudaStream_t st);
+cudaError_t launch_gather_pos(const int32_t* bfs, int64_t n, const double* flow_v,
+                              const double* omega_v, const double* p_v, double* f_pos,
+                              double* om_pos, double* p_pos, cudaStream_t st);
+cudaError_t launch_extrema(const double* flow_v, int64_t root, const double* omega, const double* p,
+                           int64_t n, double* out6, double* tmp, unsigned long long* key,
+                           cudaStream_t st);
+
+// decide.cu
+cudaError_t launch_decide(int64_t n, int64_t levels, const int64_t* level_off, int64_t max_width,
+                          const double* f_pos, const double* om0, const double* p0,
+                          const int32_t* child_lo, const int32_t* child_cnt, double thr, int64_t k,
+                          double* om, double* p, int8_t* code, int32_t* excl, double* spars,
+                          int32_t* scratch, int64_t* j_out, cudaStream_t st);
+cudaError_t launch_labels(const int8_t* code, const int32_t* pos_parent, const int32_t* bfs,
+                          int64_t n, int64_t levels, int8_t* cut_v, int64_t* eta, int64_t* labels,
+                          int32_t* lab32, int32_t* work, cudaStream_t st);
+size_t cost_work_bytes(int64_t n, int64_t k);
+cudaError_t launch_cost(const int32_t* lab32, const int32_t* parent_v, const double* flow,
+                        const double* omega, const double* p, int64_t n, int64_t k, void* work,
+                        size_t work_bytes, double* sums, double* miso, cudaStream_t st);
+}  // namespace isoc

@@ -1,0 +1,246 @@
+"""Device backend: torch CUDA tensors as buffers, libisoclust_b200.so as compute.
+
+PyTorch is plumbing only (allocation, the current stream, torch.distributed
+for the per-round key all-reduce); every arithmetic step on the hot path is
+one of our sm_100a kernels behind the C ABI.  There is no CPU path: the
+backend raises when CUDA or the library is unavailable.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+from .types import Extrema
+
+NO_KEY = 0x7FFFFFFFFFFFFFFF
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Comm:
+    """Row sharding over torch.distributed ranks (one process per GPU)."""
+
+    def __init__(self):
+        torch = _torch()
+        dist = torch.distributed
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank()
+            self.world = dist.get_world_size()
+        else:
+            self.rank, self.world = 0, 1
+        self.dist = dist
+
+    def rows(self, n: int, rank: Optional[int] = None) -> tuple[int, int]:
+        r = self.rank if rank is None else rank
+        return n * r // self.world, n * (r + 1) // self.world
+
+    def allreduce_min_(self, t) -> None:
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+
+    def allreduce_sum_(self, t) -> None:
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+
+    def allgather_rows(self, local, n: int):
+        """Concatenate per-rank row blocks (rank order) into one n-row tensor."""
+        if self.world == 1:
+            return local
+        torch = _torch()
+        sizes = [self.rows(n, r) for r in range(self.world)]
+        mx = max(h - l for l, h in sizes)
+        pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        pad[: local.shape[0]] = local
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(parts, pad)
+        return torch.cat([p[: h - l] for p, (l, h) in zip(parts, sizes)])
+
+    def allgather_stack(self, stack):
+        """Fold stacks of every rank, in rank (= row) order."""
+        if self.world == 1:
+            return stack.view(1, -1)
+        torch = _torch()
+        parts = [torch.empty_like(stack) for _ in range(self.world)]
+        self.dist.all_gather(parts, stack)
+        return torch.stack(parts)
+
+
+class CudaBackend:
+    """Stage calls into libisoclust_b200.so on torch's current CUDA stream."""
+
+    name = "cuda"
+
+    def __init__(self, device: Optional[int] = None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1702_04739_b200 needs a CUDA device (B200); no CPU fallback")
+        self.lib = _lib.load()
+        if device is not None:
+            torch.cuda.set_device(device)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.torch = torch
+
+    # -- plumbing -----------------------------------------------------
+    @property
+    def stream(self) -> ctypes.c_void_p:
+        return ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
+
+    def to_device(self, x: np.ndarray):
+        t = self.torch.from_numpy(np.ascontiguousarray(x))
+        if not t.is_pinned():
+            t = t.pin_memory()
+        return t.to(self.device, non_blocking=True)
+
+    def empty(self, shape, dtype):
+        return self.torch.empty(shape, dtype=dtype, device=self.device)
+
+    # -- exact passes -------------------------------------------------
+    def sigma_partial(self, X, n: int, d: int, lo: int, hi: int, alpha: float):
+        torch = self.torch
+        rows = hi - lo
+        stack = self.empty((_lib.FOLD_STACK_BYTES,), torch.uint8)
+        nn_j = self.empty((rows,), torch.int32)
+        nn_d = self.empty((rows,), torch.float64)
+        nn_tie = self.empty((rows,), torch.int8)
+        p = self.empty((rows,), torch.float64)
+        check(self.lib.isoc_sigma_partial(_ptr(X), n, d, lo, hi, float(alpha), _ptr(stack),
+                                          _ptr(nn_j), _ptr(nn_d), _ptr(nn_tie), _ptr(p), self.stream))
+        return stack, (nn_j, nn_d, nn_tie), p
+
+    def sigma_finish(self, stacks) -> float:
+        total = ctypes.c_double(0.0)
+        check(self.lib.isoc_sigma_finish(_ptr(stacks), stacks.shape[0], ctypes.byref(total),
+                                         self.stream))
+        return total.value
+
+    def omega(self, X, n: int, d: int, lo: int, hi: int, sigma: float):
+        out = self.empty((hi - lo,), self.torch.float64)
+        check(self.lib.isoc_omega(_ptr(X), n, d, lo, hi, float(sigma), _ptr(out), self.stream))
+        return out
+
+    # -- Boruvka ------------------------------------------------------
+    def mst_create(self, X, n: int, d: int, lo: int, hi: int):
+        h = ctypes.c_void_p()
+        check(self.lib.isoc_mst_create(_ptr(X), n, d, lo, hi, self.stream, ctypes.byref(h)))
+        return h
+
+    def mst_round(self, h, n: int, comm: Comm, nn=None):
+        torch = self.torch
+        cmin = self.empty((n,), torch.int64)
+        cedge = self.empty((n,), torch.int64)
+        if nn is not None:
+            check(self.lib.isoc_mst_round_local(h, 1, _ptr(nn[0]), _ptr(nn[1]), _ptr(nn[2]), _ptr(cmin)))
+        else:
+            check(self.lib.isoc_mst_round_local(h, 0, None, None, None, _ptr(cmin)))
+        comm.allreduce_min_(cmin)
+        check(self.lib.isoc_mst_round_edges(h, _ptr(cmin), _ptr(cedge)))
+        comm.allreduce_min_(cedge)
+        comps, ties, rescans = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(self.lib.isoc_mst_round_finish(h, _ptr(cmin), _ptr(cedge), ctypes.byref(comps),
+                                             ctypes.byref(ties), ctypes.byref(rescans)))
+        return comps.value, ties.value, rescans.value
+
+    def mst_edges(self, h, n: int):
+        torch = self.torch
+        u = self.empty((n - 1,), torch.int32)
+        v = self.empty((n - 1,), torch.int32)
+        w = self.empty((n - 1,), torch.float64)
+        check(self.lib.isoc_mst_edges(h, _ptr(u), _ptr(v), _ptr(w)))
+        return u, v, w
+
+    def mst_destroy(self, h) -> None:
+        self.lib.isoc_mst_destroy(h)
+
+    # -- trees ----------------------------------------------------------
+    def tree_from_edges(self, u, v, w, n: int, root: int, sigma: float) -> "DeviceTree":
+        h = ctypes.c_void_p()
+        check(self.lib.isoc_tree_from_edges(_ptr(u), _ptr(v), _ptr(w), n, root, float(sigma),
+                                             self.stream, ctypes.byref(h)))
+        return DeviceTree(self, h, n)
+
+    def tree_from_parent(self, parent: np.ndarray, flows: np.ndarray, root: int,
+                         child_id: Optional[np.ndarray] = None) -> "DeviceTree":
+        n = parent.shape[0]
+        par = self.to_device(np.ascontiguousarray(parent, dtype=np.int64))
+        fl = self.to_device(np.ascontiguousarray(flows, dtype=np.float64))
+        cid = None if child_id is None else self.to_device(np.ascontiguousarray(child_id, dtype=np.int64))
+        h = ctypes.c_void_p()
+        check(self.lib.isoc_tree_from_parent(_ptr(par), _ptr(fl), None if cid is None else _ptr(cid),
+                                             n, root, self.stream, ctypes.byref(h)))
+        return DeviceTree(self, h, n)
+
+
+@dataclass
+class Witness:
+    labels: np.ndarray
+    cut: np.ndarray
+    eta: np.ndarray
+    sparsities: list
+    miso: float
+
+
+class DeviceTree:
+    """Owner of an isoc_tree handle (BFS-position layout on the device)."""
+
+    def __init__(self, backend: CudaBackend, handle, n: int):
+        self.b = backend
+        self.h = handle
+        self.n = n
+        self.weights_set = False
+
+    def __del__(self):
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            try:
+                self.b.lib.isoc_tree_destroy(h)
+            except Exception:
+                pass
+
+    def export(self):
+        n = self.n
+        parent = np.empty(n, np.int64)
+        flow = np.empty(n, np.float64)
+        depth = np.empty(n, np.int64)
+        cid = np.empty(n, np.int64)
+        order = np.empty(n, np.int64)
+        pdist = np.empty(n, np.float64)
+        md = ctypes.c_int64()
+        check(self.b.lib.isoc_tree_export(self.h, parent.ctypes.data, flow.ctypes.data, depth.ctypes.data,
+                                          cid.ctypes.data, order.ctypes.data, ctypes.byref(md),
+                                          pdist.ctypes.data))
+        return parent, flow, depth, cid, order, int(md.value), pdist
+
+    def set_weights(self, omega_dev, p_dev) -> Extrema:
+        ext = np.empty(6, np.float64)
+        check(self.b.lib.isoc_tree_set_weights(self.h, _ptr(omega_dev), _ptr(p_dev), ext.ctypes.data))
+        self.weights_set = True
+        return Extrema(*[float(v) for v in ext])
+
+    def decide(self, N: float, k: int, slot: int) -> int:
+        j = ctypes.c_int64()
+        check(self.b.lib.isoc_decide(self.h, float(N), int(k), int(slot), ctypes.byref(j)))
+        return int(j.value)
+
+    def witness(self, slot: int, k: int) -> Witness:
+        n = self.n
+        labels = np.empty(n, np.int64)
+        cut = np.empty(n, np.int8)
+        eta = np.empty(n, np.int64)
+        sp = np.empty(k, np.float64)
+        miso = ctypes.c_double()
+        check(self.b.lib.isoc_witness(self.h, int(slot), int(k), labels.ctypes.data, cut.ctypes.data,
+                                      eta.ctypes.data, sp.ctypes.data, ctypes.byref(miso)))
+        return Witness(labels, cut, eta, [float(v) for v in sp], float(miso.value))

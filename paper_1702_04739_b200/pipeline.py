@@ -1,0 +1,448 @@
+"""Drop-in clustering entry point and stage API on the B200 path.
+
+`run_pipeline` keeps the reference signature and result type
+(/root/reference/pkg/src/isoclust/pipeline.py:41-104): points and k in;
+cluster labels (1..k), the residual mask (labels == 0) and the k-th
+isoperimetric value (result.miso) out, plus the same four timing buckets.
+Stages:
+  affinity   K1 exact sigma pass (+ exact nearest neighbours = Boruvka
+             round 1) and K2 exact omega pass       affinity.py:124-279
+  mst        Boruvka rounds (FP32 filter + exact re-rank), rooting,
+             parent flows                            mst.py:128-181
+  partition  bisection over device decision sweeps   isoperim.py:222-308
+Under torch.distributed (one process per GPU) rows are sharded for the
+dense stages; the per-round Boruvka keys are MIN-all-reduced and the tree
+phase runs replicated on every rank.  Results do not depend on the number of
+GPUs.
+
+The dense distance matrix of the reference is never formed, so the
+reference's n <= 46,340 cap (affinity.py:23-24) does not apply.
+"""
+from __future__ import annotations
+
+import math
+import os
+import time
+import warnings
+from typing import Callable, Optional, Union
+
+import numpy as np
+
+from ._lib import InfeasibleSubpartitionError
+from .engine import Comm, CudaBackend, DeviceTree
+from .types import (
+    BRACKET_EPS,
+    MAX_ITERATIONS,
+    NO_VERTEX,
+    DecisionOutcome,
+    Extrema,
+    MisoResult,
+    NodeWeights,
+    PipelineRun,
+    RootedTree,
+)
+
+ENGINES = ("seq", "par")
+WORKERS_ENV_VAR = "ISOCLUST_WORKERS"
+
+_BACKEND: Optional[CudaBackend] = None
+
+
+def backend() -> CudaBackend:
+    global _BACKEND
+    if _BACKEND is None:
+        _BACKEND = CudaBackend()
+    return _BACKEND
+
+
+def resolve_workers(workers: Optional[int] = None) -> int:
+    """_primitives.py:25-41 (the count is recorded; it never changes results)."""
+    if workers is None:
+        env = os.environ.get(WORKERS_ENV_VAR, "").strip()
+        if env:
+            try:
+                workers = int(env)
+            except ValueError:
+                raise ValueError(f"{WORKERS_ENV_VAR} must be an integer, got {env!r}") from None
+        else:
+            workers = os.cpu_count() or 1
+    workers = int(workers)
+    if workers < 1:
+        raise ValueError(f"worker count must be >= 1, got {workers}")
+    return workers
+
+
+def _validate_points(points) -> np.ndarray:
+    """affinity.py:70-81."""
+    x = np.ascontiguousarray(points, dtype=np.float64)
+    if x.ndim != 2:
+        raise ValueError(f"points must be a 2-d array, got shape {x.shape}")
+    n, d = x.shape
+    if n < 2:
+        raise ValueError(f"need at least 2 points, got {n}")
+    if d < 1:
+        raise ValueError("points must have at least one coordinate")
+    if not np.isfinite(x).all():
+        raise ValueError("points must be finite")
+    return x
+
+
+def _validate_k(k) -> None:
+    """isoperim.py:71-79."""
+    if not isinstance(k, (int, np.integer)) or isinstance(k, bool):
+        raise TypeError(f"k must be an integer, got {k!r}")
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+
+
+# --------------------------------------------------------------- stages
+class _Points:
+    """Points resident on the device plus this rank's row shard."""
+
+    def __init__(self, points, comm: Optional[Comm] = None, b: Optional[CudaBackend] = None):
+        self.b = b or backend()
+        self.comm = comm or Comm()
+        self.host = _validate_points(points)
+        self.n, self.d = self.host.shape
+        self.lo, self.hi = self.comm.rows(self.n)
+        self.X = self.b.to_device(self.host)
+
+
+def _sigma_pass(P: _Points, alpha: float):
+    stack, nn, p_loc = P.b.sigma_partial(P.X, P.n, P.d, P.lo, P.hi, alpha)
+    return stack, nn, p_loc
+
+
+def _sigma_from_stack(P: _Points, stack) -> float:
+    total = P.b.sigma_finish(P.comm.allgather_stack(stack))
+    n = P.n
+    mean = total / (n * (n - 1))
+    if not (mean > 0):
+        raise ValueError("all points coincide; no usable distance scale")
+    return mean
+
+
+def _boruvka(P: _Points, nn=None) -> tuple:
+    """MST edges on the device; returns (u, v, w, stats)."""
+    b, comm, n = P.b, P.comm, P.n
+    h = b.mst_create(P.X, n, P.d, P.lo, P.hi)
+    try:
+        comps, rounds, ties, rescans = n, 0, 0, 0
+        while comps > 1:
+            c, t, r = b.mst_round(h, n, comm, nn if rounds == 0 else None)
+            rounds += 1
+            ties += t
+            rescans += r
+            if c >= comps:
+                raise RuntimeError(f"Boruvka round {rounds} made no progress ({c} components)")
+            comps = c
+        u, v, w = b.mst_edges(h, n)
+    finally:
+        b.mst_destroy(h)
+    if comm.world > 1:
+        import torch
+
+        tt = torch.tensor([ties, rescans], dtype=torch.int64, device=b.device)
+        comm.allreduce_sum_(tt)
+        ties, rescans = (int(x) for x in tt.tolist())
+    if ties:
+        warnings.warn(
+            f"{ties} exact distance ties at a component minimum: the MST may differ from the "
+            "reference's Prim tie rule (SURVEY 8c, Appendix A.6)", RuntimeWarning, stacklevel=3)
+    return u, v, w, {"boruvka_rounds": rounds, "exact_ties": ties, "exact_rescans": rescans}
+
+
+def _rooted_tree_view(dt: DeviceTree, root: int) -> RootedTree:
+    parent, flow, depth, cid, order, max_depth, _ = dt.export()
+    return RootedTree(parent, flow, depth, cid, order, int(root), max_depth, _device=dt)
+
+
+def auto_sigma(points) -> float:
+    """Mean off-diagonal distance (affinity.py:233-241), matrix-free, bitwise."""
+    P = _Points(points)
+    stack, _, _ = _sigma_pass(P, 0.0)
+    return _sigma_from_stack(P, stack)
+
+
+def node_weights(points, sigma: float, alpha: float = 0.0) -> NodeWeights:
+    """vertex_weights + potentials (affinity.py:175-257) from points."""
+    if not (sigma > 0):
+        raise ValueError(f"sigma must be > 0, got {sigma}")
+    if alpha < 0:
+        raise ValueError(f"alpha must be >= 0, got {alpha}")
+    P = _Points(points)
+    om = P.comm.allgather_rows(P.b.omega(P.X, P.n, P.d, P.lo, P.hi, sigma), P.n)
+    if alpha > 0:
+        _, _, p_loc = _sigma_pass(P, alpha)
+        p = P.comm.allgather_rows(p_loc, P.n).cpu().numpy()
+    else:
+        p = np.zeros(P.n)
+    return NodeWeights(omega=om.cpu().numpy(), p=p, sigma=float(sigma), alpha=float(alpha))
+
+
+def minimum_spanning_tree(points, sigma: float, root: int = 0) -> RootedTree:
+    """prim_mst (mst.py:128-181) from points: Boruvka on the device, rooted."""
+    if not (sigma > 0):
+        raise ValueError(f"sigma must be > 0, got {sigma}")
+    P = _Points(points)
+    if not (0 <= root < P.n):
+        raise ValueError(f"root must be in [0, {P.n}), got {root}")
+    u, v, w, _ = _boruvka(P)
+    dt = P.b.tree_from_edges(u, v, w, P.n, root, sigma)
+    return _rooted_tree_view(dt, root)
+
+
+# mst.py name of the stage this replaces
+prim_mst = minimum_spanning_tree
+
+
+def total_distance(tree: RootedTree) -> float:
+    """Tree weight (mst.py:184-187): fsum of the exact parent-edge distances."""
+    dt = _device_tree(tree)
+    pdist = dt.export()[6]
+    nonroot = np.flatnonzero(tree.parent != NO_VERTEX)
+    return math.fsum(float(pdist[u]) for u in nonroot)
+
+
+def tree_from_parent_list(parent, parent_flow, root: Optional[int] = None) -> RootedTree:
+    """mst.py:78-125 on the device (sibling ranks by ascending vertex index)."""
+    par = np.asarray(parent, dtype=np.int64).copy()
+    flows = np.asarray(parent_flow, dtype=np.float64).copy()
+    n = par.shape[0]
+    if par.ndim != 1 or flows.shape != par.shape:
+        raise ValueError("parent and parent_flow must be 1-d arrays of equal length")
+    roots = np.flatnonzero(par == NO_VERTEX)
+    if root is None:
+        if roots.size != 1:
+            raise ValueError(f"expected exactly one root sentinel, found {roots.size}")
+        root = int(roots[0])
+    elif roots.size != 1 or int(roots[0]) != root:
+        raise ValueError("root does not match the parent array's sentinel")
+    if (par[np.arange(n) != root] < 0).any() or (par >= n).any():
+        raise ValueError("parent indices out of range")
+    dt = backend().tree_from_parent(par, flows, root)
+    return _rooted_tree_view(dt, root)
+
+
+def _device_tree(tree: RootedTree) -> DeviceTree:
+    if tree._device is None:
+        tree._device = backend().tree_from_parent(tree.parent, tree.parent_flow, tree.root,
+                                                  child_id=tree.child_id)
+    return tree._device
+
+
+def extrema(tree: RootedTree, weights: NodeWeights) -> Extrema:
+    """affinity.py:260-279 on the device (pow2 folds, bitwise)."""
+    if tree.n != weights.n:
+        raise ValueError(f"tree has {tree.n} vertices but weights have {weights.n}")
+    dt = _device_tree(tree)
+    b = dt.b
+    return dt.set_weights(b.to_device(weights.omega), b.to_device(weights.p))
+
+
+def _attach(tree: RootedTree, weights: NodeWeights) -> DeviceTree:
+    dt = _device_tree(tree)
+    if getattr(dt, "_weights_id", None) is not weights:
+        b = dt.b
+        dt.set_weights(b.to_device(weights.omega), b.to_device(weights.p))
+        dt._weights_id = weights
+    return dt
+
+
+def _outcome(dt: DeviceTree, slot: int, k: int, j: int) -> tuple[DecisionOutcome, np.ndarray, float]:
+    w = dt.witness(slot, k)
+    out = DecisionOutcome(feasible=(j == k), clusters_found=j, cut=w.cut, eta=w.eta,
+                          cluster_sparsities=w.sparsities[:j])
+    return out, w.labels, w.miso
+
+
+def decide(tree: RootedTree, weights: NodeWeights, k: int, N: float) -> DecisionOutcome:
+    """One decision sweep (isoperim.py:82-144) on the device."""
+    _validate_k(k)
+    if tree.n != weights.n:
+        raise ValueError(f"tree has {tree.n} vertices but weights have {weights.n}")
+    if not math.isfinite(N):
+        raise ValueError(f"threshold must be finite, got {N}")
+    dt = _attach(tree, weights)
+    j = dt.decide(N, k, 0)
+    return _outcome(dt, 0, k, j)[0]
+
+
+par_decide = decide
+
+
+def run_bisection(dt: DeviceTree, ext: Extrema, k: int, n: int) -> MisoResult:
+    """isoperim.py:222-308 with device decision sweeps.
+
+    Same closed-form bracket, round budget, stop test, midpoint expression,
+    witness rule and infeasible fallbacks as the reference; the witness's
+    labels and exact cost are computed on the device once at the end.
+    """
+    _validate_k(k)
+    alpha0 = (ext.phi_star_min + ext.p_star_min) / ext.omega_star_sum
+    beta0 = (ext.phi_star_sum + ext.p_star_sum) / ext.omega_star_min
+    if beta0 > alpha0:
+        t_gap = math.ceil(
+            math.log2(2.0 * ext.omega_star_sum**2 * (beta0 - alpha0))
+            - math.log2(ext.phi_star_min + ext.p_star_min)
+        )
+        t_eps = math.ceil(math.log2((beta0 - alpha0) / (BRACKET_EPS * max(1.0, beta0))))
+        t = max(t_gap, t_eps)
+    else:
+        t = 1
+    t = min(MAX_ITERATIONS, max(1, t))
+
+    alpha, beta = alpha0, beta0
+    wslot: Optional[int] = None
+    wj = 0
+    rounds = 0
+    trace: list = []
+
+    def sweep(N: float) -> tuple[bool, int, int]:
+        slot = 0 if wslot is None else 1 - wslot
+        j = dt.decide(N, k, slot)
+        return j == k, j, slot
+
+    for _ in range(t):
+        if beta - alpha <= BRACKET_EPS * max(1.0, beta):
+            break
+        mid = (alpha + beta) / 2.0
+        ok, j, slot = sweep(mid)
+        rounds += 1
+        trace.append((mid, ok))
+        if ok:
+            beta = mid
+            wslot, wj = slot, j
+        else:
+            alpha = mid
+
+    if wslot is None:
+        ok, j, slot = sweep(beta0)
+        rounds += 1
+        trace.append((beta0, ok))
+        if not ok:
+            bumped = beta0 * (1.0 + 1e-12)
+            ok, j, slot = sweep(bumped)
+            rounds += 1
+            trace.append((bumped, ok))
+        if not ok:
+            raise InfeasibleSubpartitionError(
+                f"no feasible {k}-subpartition found within bracket (n={n}, k={k})"
+            )
+        wslot, wj = slot, j
+
+    outcome, labels, miso = _outcome(dt, wslot, k, wj)
+    return MisoResult(miso=miso, labels=labels, outcome=outcome, iterations=rounds,
+                      alpha_final=alpha, beta_final=beta, trace=trace)
+
+
+def solve_miso(tree: RootedTree, weights: NodeWeights, ext: Extrema, k: int) -> MisoResult:
+    """Exact k-th isoperimetric number of the tree (isoperim.py:311-321)."""
+    _validate_k(k)
+    if tree.n != weights.n:
+        raise ValueError(f"tree has {tree.n} vertices but weights have {weights.n}")
+    dt = _attach(tree, weights)
+    return run_bisection(dt, ext, k, tree.n)
+
+
+def par_solve_miso(tree: RootedTree, weights: NodeWeights, ext: Extrema, k: int, *,
+                   workers: Optional[int] = None) -> MisoResult:
+    """parengine.py:212-232: same device engine (workers never change results)."""
+    return solve_miso(tree, weights, ext, k)
+
+
+# -------------------------------------------------------------- pipeline
+def run_pipeline(
+    points: np.ndarray,
+    k: int,
+    sigma: Union[str, float] = "auto",
+    alpha: float = 0.0,
+    root: int = 0,
+    engine: str = "seq",
+    workers: Optional[int] = None,
+) -> PipelineRun:
+    """Cluster a point set into k groups; returns the result with timings.
+
+    Same contract as the reference (pipeline.py:41-104).  `engine` accepts
+    "seq" and "par" (both run the device engine and return identical
+    results); `workers` is recorded but, as in the reference, never changes
+    results.  Under torch.distributed, every rank returns the same run.
+    """
+    if engine not in ENGINES:
+        raise ValueError(f"engine must be one of {ENGINES}, got {engine!r}")
+    x = np.asarray(points, dtype=np.float64)
+    n, d = x.shape if x.ndim == 2 else (0, 0)
+    nworkers = resolve_workers(workers) if engine == "par" else 1
+    b = backend()
+    torch = b.torch
+
+    t_start = time.perf_counter()
+    t0 = time.perf_counter()
+    P = _Points(x, b=b)
+    need_pass = sigma == "auto" or alpha > 0
+    nn = None
+    p_loc = None
+    if need_pass:
+        stack, nn, p_loc = _sigma_pass(P, float(alpha) if alpha > 0 else 0.0)
+        sigma_val = _sigma_from_stack(P, stack) if sigma == "auto" else float(sigma)
+    else:
+        sigma_val = float(sigma)
+    if not (sigma_val > 0):
+        raise ValueError(f"sigma must be > 0, got {sigma_val}")
+    affinity_ms = (time.perf_counter() - t0) * 1e3
+
+    t0 = time.perf_counter()
+    if not (0 <= root < n):
+        raise ValueError(f"root must be in [0, {n}), got {root}")
+    u, v, w, stats = _boruvka(P, nn)
+    dt = b.tree_from_edges(u, v, w, n, root, sigma_val)
+    torch.cuda.synchronize()
+    mst_ms = (time.perf_counter() - t0) * 1e3
+
+    t0 = time.perf_counter()
+    if alpha < 0:
+        raise ValueError(f"alpha must be >= 0, got {alpha}")
+    om = P.comm.allgather_rows(b.omega(P.X, n, d, P.lo, P.hi, sigma_val), n)
+    if alpha > 0:
+        p = P.comm.allgather_rows(p_loc, n)
+    else:
+        p = torch.zeros(n, dtype=torch.float64, device=b.device)
+    ext = dt.set_weights(om, p)
+    affinity_ms += (time.perf_counter() - t0) * 1e3
+
+    t0 = time.perf_counter()
+    result = run_bisection(dt, ext, k, n)
+    partition_ms = (time.perf_counter() - t0) * 1e3
+    total_ms = (time.perf_counter() - t_start) * 1e3
+
+    return PipelineRun(
+        result=result, n=n, d=d, k=k, sigma=sigma_val, alpha=float(alpha), root=root,
+        engine=engine, workers=nworkers,
+        timings_ms={"affinity": affinity_ms, "mst": mst_ms, "partition": partition_ms,
+                    "total": total_ms},
+        gpus=P.comm.world, mst_stats=stats,
+    )
+
+
+def summarize(run: PipelineRun) -> dict:
+    """JSON-ready summary (schema version 1, pipeline.py:107-128)."""
+    labels = run.result.labels
+    cluster_sizes = [int(np.sum(labels == c)) for c in range(1, run.k + 1)]
+    return {
+        "schema": 1,
+        "n": run.n,
+        "d": run.d,
+        "k": run.k,
+        "miso": run.result.miso,
+        "iterations": run.result.iterations,
+        "alpha_final": run.result.alpha_final,
+        "beta_final": run.result.beta_final,
+        "cluster_sizes": cluster_sizes,
+        "residual_count": int(np.sum(labels == 0)),
+        "sigma": run.sigma,
+        "alpha": run.alpha,
+        "root": run.root,
+        "engine": run.engine,
+        "workers": run.workers,
+        "timings_ms": {k: round(v, 3) for k, v in run.timings_ms.items()},
+    }
