@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libisoclust_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 ISOC_OK, ISOC_EINVAL, ISOC_ETYPE, ISOC_EINFEASIBLE, ISOC_ENOMEM, ISOC_ECUDA = range(6)
-FOLD_STACK_BYTES = 1160
+FOLD_STACK_BYTES = 1544
 
 _lock = threading.Lock()
 _lib = None

@@ -118,26 +118,27 @@ int isoc_sigma_partial(const double* X, int64_t n, int32_t d, int64_t lo, int64_
     const int64_t rows = hi - lo;
     const int want_p = alpha > 0.0;
     double* row_vals = nullptr;
-    int32_t *row_deps = nullptr, *row_cnt = nullptr, *flags = nullptr, *sdep = nullptr;
+    int32_t *row_cnt = nullptr, *flags = nullptr;
+    uint64_t *row_ids = nullptr, *sid = nullptr;
     double* sval = nullptr;
     int8_t* sown = nullptr;
     FoldStack* groups = nullptr;
     CK(aalloc(&row_vals, sigma_rowstack_entries(rows), st));
-    CK(aalloc(&row_deps, sigma_rowstack_entries(rows), st));
+    CK(aalloc(&row_ids, sigma_rowstack_entries(rows), st));
     CK(aalloc(&row_cnt, rows, st));
     CK(aalloc(&flags, 1, st));
     CK(aalloc(&sval, rows, st));
-    CK(aalloc(&sdep, rows, st));
+    CK(aalloc(&sid, rows, st));
     CK(aalloc(&sown, rows, st));
     const int64_t ng = (rows + 63) / 64;
     CK(aalloc(&groups, ng, st));
     CK(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
     CK(cudaMemsetAsync(sown, 0, rows, st));
-    CK(launch_sigma_pass(X, n, d, lo, hi, want_p, row_vals, row_deps, row_cnt, flags, nn_j, nn_d,
+    CK(launch_sigma_pass(X, n, d, lo, hi, want_p, row_vals, row_ids, row_cnt, flags, nn_j, nn_d,
                          nn_tie, want_p ? p_dev : nullptr, st));
     const int64_t b_hi = hi < n ? hi + 1 : n;  // boundaries lo+1 .. min(hi, n-1)
-    CK(launch_sigma_straddle(X, n, d, lo + 1, b_hi, sval, sdep, sown, st));
-    CK(launch_sigma_merge_rows(n, lo, hi, 64, row_vals, row_deps, row_cnt, sval, sdep, sown, groups,
+    CK(launch_sigma_straddle(X, n, d, lo + 1, b_hi, sval, sid, sown, st));
+    CK(launch_sigma_merge_rows(n, lo, hi, 64, row_vals, row_ids, row_cnt, sval, sid, sown, groups,
                                flags, st));
     CK(fold_stacks(groups, ng, reinterpret_cast<FoldStack*>(stack_dev), flags, st));
     if (want_p) {
@@ -148,8 +149,8 @@ int isoc_sigma_partial(const double* X, int64_t n, int32_t d, int64_t lo, int64_
     }
     int32_t hflags = 0;
     CK(cudaMemcpyAsync(&hflags, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(row_vals, st); cudaFreeAsync(row_deps, st); cudaFreeAsync(row_cnt, st);
-    cudaFreeAsync(sval, st); cudaFreeAsync(sdep, st); cudaFreeAsync(sown, st);
+    cudaFreeAsync(row_vals, st); cudaFreeAsync(row_ids, st); cudaFreeAsync(row_cnt, st);
+    cudaFreeAsync(sval, st); cudaFreeAsync(sid, st); cudaFreeAsync(sown, st);
     cudaFreeAsync(groups, st); cudaFreeAsync(flags, st);
     CK(cudaStreamSynchronize(st));
     if (hflags) return fail(ISOC_ECUDA, "pairwise fold stack overflow (flags=%d)", hflags);
@@ -170,9 +171,9 @@ int isoc_sigma_finish(const void* stacks_dev, int64_t nseg, double* total_host, 
     cudaFreeAsync(out, st);
     cudaFreeAsync(flags, st);
     CK(cudaStreamSynchronize(st));
-    if (h.count != 1 || h.depth[0] != 0 || h.overflow)
-        return fail(ISOC_EINVAL, "fold stacks do not close to one root (count=%d depth=%d)", h.count,
-                    h.count > 0 ? h.depth[0] : -1);
+    if (h.count != 1 || h.id[0] != 1 || h.overflow)
+        return fail(ISOC_EINVAL, "fold stacks do not close to one root (count=%d id=%llu)", h.count,
+                    h.count > 0 ? (unsigned long long)h.id[0] : 0ull);
     *total_host = 0.0 + h.value[0];
     return ISOC_OK;
 }

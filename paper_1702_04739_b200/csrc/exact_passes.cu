@@ -30,8 +30,8 @@ constexpr int XN = 128;       // columns per tile
 constexpr int XK = 16;        // k chunk
 constexpr int XT = 256;       // threads
 constexpr int RING = 256;     // ring columns (two tiles)
-constexpr int ROW_CAP = 48;   // per-row stack capacity
-constexpr int PC_LEVELS = 40; // binary-counter levels for pow2 row folds
+constexpr int ROW_CAP = 40;   // per-row stack capacity (<= 2 log2(n/64) + 2 used)
+constexpr int PC_LEVELS = 32; // binary-counter levels for pow2 row folds
 
 struct TileSmem {
     double As[XK][XM];
@@ -139,11 +139,11 @@ struct SigmaSmem {
     TileSmem tile;
     double ring[XM][RING];
     double st_val[XM][ROW_CAP];
-    int32_t st_dep[XM][ROW_CAP];
+    uint64_t st_id[XM][ROW_CAP];
     double pc[XM][PC_LEVELS];
     int64_t lf_start[XM];
     int32_t lf_len[XM];
-    int32_t lf_dep[XM];
+    uint64_t lf_id[XM];
     int32_t lf_done[XM];
     int32_t st_cnt[XM];
     int32_t st_ovf[XM];
@@ -151,7 +151,7 @@ struct SigmaSmem {
 
 __global__ void __launch_bounds__(XT, 2)
 sigma_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo, int64_t row_hi,
-                  int want_p, double* __restrict__ row_vals, int32_t* __restrict__ row_deps,
+                  int want_p, double* __restrict__ row_vals, uint64_t* __restrict__ row_ids,
                   int32_t* __restrict__ row_cnt, int32_t* __restrict__ flags,
                   int32_t* __restrict__ nn_j, double* __restrict__ nn_d, int8_t* __restrict__ nn_tie,
                   double* __restrict__ pfold) {
@@ -174,7 +174,7 @@ sigma_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo
                 done = 0;
                 sm.lf_start[tid] = L.start;
                 sm.lf_len[tid] = (int32_t)L.len;
-                sm.lf_dep[tid] = L.depth;
+                sm.lf_id[tid] = L.hid;
             }
         }
         sm.lf_done[tid] = done;
@@ -271,7 +271,7 @@ sigma_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo
                                 res = __dadd_rn(res, sm.ring[r][(ls + i) & (RING - 1)]);
                         }
                         int cnt = sm.st_cnt[r], ovf = sm.st_ovf[r];
-                        stack_push(sm.st_val[r], sm.st_dep[r], cnt, ROW_CAP, ovf, res, sm.lf_dep[r]);
+                        stack_push(sm.st_val[r], sm.st_id[r], cnt, ROW_CAP, ovf, res, sm.lf_id[r]);
                         sm.st_cnt[r] = cnt;
                         sm.st_ovf[r] = ovf;
                         int64_t end = sm.lf_start[r] + sm.lf_len[r];
@@ -284,7 +284,7 @@ sigma_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo
                             } else {
                                 sm.lf_start[r] = L.start;
                                 sm.lf_len[r] = (int32_t)L.len;
-                                sm.lf_dep[r] = L.depth;
+                                sm.lf_id[r] = L.hid;
                             }
                         }
                     }
@@ -316,7 +316,7 @@ sigma_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo
         if (row < row_hi && s < sm.st_cnt[r]) {
             int64_t li = row - row_lo;
             row_vals[li * ROW_CAP + s] = sm.st_val[r][s];
-            row_deps[li * ROW_CAP + s] = sm.st_dep[r][s];
+            row_ids[li * ROW_CAP + s] = sm.st_id[r][s];
         }
     }
     if (tid < XM) {
@@ -333,7 +333,7 @@ sigma_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo
 // starts inside row b-1.  One warp per boundary.
 __global__ void sigma_straddle_kernel(const double* __restrict__ X, int64_t n, int d,
                                       int64_t b_lo, int64_t b_hi, double* __restrict__ sval,
-                                      int32_t* __restrict__ sdep, int8_t* __restrict__ sown) {
+                                      uint64_t* __restrict__ sid, int8_t* __restrict__ sown) {
     const int lane = threadIdx.x & 31;
     const int64_t b = b_lo + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (b >= b_hi) return;
@@ -370,7 +370,7 @@ __global__ void sigma_straddle_kernel(const double* __restrict__ X, int64_t n, i
     double res = np_leaf_sum(get, L.len);
     if (lane == 0) {
         sval[b - b_lo] = res;
-        sdep[b - b_lo] = L.depth;
+        sid[b - b_lo] = L.hid;
         sown[b - b_lo] = 1;
     }
 }
@@ -380,10 +380,10 @@ __global__ void sigma_straddle_kernel(const double* __restrict__ X, int64_t n, i
 // the last group also appends straddle(hi) (hi < n).
 __global__ void sigma_merge_rows_kernel(int64_t n, int64_t lo, int64_t hi, int G,
                                         const double* __restrict__ row_vals,
-                                        const int32_t* __restrict__ row_deps,
+                                        const uint64_t* __restrict__ row_ids,
                                         const int32_t* __restrict__ row_cnt,
                                         const double* __restrict__ sval,
-                                        const int32_t* __restrict__ sdep,
+                                        const uint64_t* __restrict__ sid,
                                         const int8_t* __restrict__ sown,
                                         FoldStack* __restrict__ out, int32_t* __restrict__ flags) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -394,15 +394,15 @@ __global__ void sigma_merge_rows_kernel(int64_t n, int64_t lo, int64_t hi, int G
     const int64_t a = lo + g * G, b = (a + G < hi) ? a + G : hi;
     for (int64_t i = a; i < b; ++i) {
         if (i > lo && sown[i - lo - 1])
-            stack_push(S.value, S.depth, cnt, kStackCap, ovf, sval[i - lo - 1], sdep[i - lo - 1]);
+            stack_push(S.value, S.id, cnt, kStackCap, ovf, sval[i - lo - 1], sid[i - lo - 1]);
         const int64_t li = i - lo;
         const int c = row_cnt[li];
         for (int s = 0; s < c; ++s)
-            stack_push(S.value, S.depth, cnt, kStackCap, ovf, row_vals[li * ROW_CAP + s],
-                       row_deps[li * ROW_CAP + s]);
+            stack_push(S.value, S.id, cnt, kStackCap, ovf, row_vals[li * ROW_CAP + s],
+                       row_ids[li * ROW_CAP + s]);
     }
     if (b == hi && hi < n && sown[hi - lo - 1])
-        stack_push(S.value, S.depth, cnt, kStackCap, ovf, sval[hi - lo - 1], sdep[hi - lo - 1]);
+        stack_push(S.value, S.id, cnt, kStackCap, ovf, sval[hi - lo - 1], sid[hi - lo - 1]);
     S.count = cnt;
     S.overflow = ovf;
     if (ovf) atomicOr(flags, 2);
@@ -420,7 +420,7 @@ __global__ void stack_merge_kernel(const FoldStack* __restrict__ in, int64_t nin
         const FoldStack& I = in[q];
         ovf |= I.overflow;
         for (int s = 0; s < I.count; ++s)
-            stack_push(S.value, S.depth, cnt, kStackCap, ovf, I.value[s], I.depth[s]);
+            stack_push(S.value, S.id, cnt, kStackCap, ovf, I.value[s], I.id[s]);
     }
     S.count = cnt;
     S.overflow = ovf;
@@ -480,7 +480,7 @@ omega_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo
 size_t sigma_rowstack_entries(int64_t rows) { return (size_t)rows * ROW_CAP; }
 
 cudaError_t launch_sigma_pass(const double* X, int64_t n, int d, int64_t lo, int64_t hi,
-                              int want_p, double* row_vals, int32_t* row_deps, int32_t* row_cnt,
+                              int want_p, double* row_vals, uint64_t* row_ids, int32_t* row_cnt,
                               int32_t* flags, int32_t* nn_j, double* nn_d, int8_t* nn_tie,
                               double* pfold, cudaStream_t st) {
     const int64_t rows = hi - lo;
@@ -490,29 +490,29 @@ cudaError_t launch_sigma_pass(const double* X, int64_t n, int d, int64_t lo, int
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((rows + XM - 1) / XM);
-    sigma_pass_kernel<<<grid, XT, smem, st>>>(X, n, d, lo, hi, want_p, row_vals, row_deps, row_cnt,
+    sigma_pass_kernel<<<grid, XT, smem, st>>>(X, n, d, lo, hi, want_p, row_vals, row_ids, row_cnt,
                                               flags, nn_j, nn_d, nn_tie, pfold);
     return cudaGetLastError();
 }
 
 cudaError_t launch_sigma_straddle(const double* X, int64_t n, int d, int64_t b_lo, int64_t b_hi,
-                                  double* sval, int32_t* sdep, int8_t* sown, cudaStream_t st) {
+                                  double* sval, uint64_t* sid, int8_t* sown, cudaStream_t st) {
     const int64_t nb = b_hi - b_lo;
     if (nb <= 0) return cudaSuccess;
     const unsigned grid = (unsigned)((nb * 32 + 255) / 256);
-    sigma_straddle_kernel<<<grid, 256, 0, st>>>(X, n, d, b_lo, b_hi, sval, sdep, sown);
+    sigma_straddle_kernel<<<grid, 256, 0, st>>>(X, n, d, b_lo, b_hi, sval, sid, sown);
     return cudaGetLastError();
 }
 
 cudaError_t launch_sigma_merge_rows(int64_t n, int64_t lo, int64_t hi, int G,
-                                    const double* row_vals, const int32_t* row_deps,
+                                    const double* row_vals, const uint64_t* row_ids,
                                     const int32_t* row_cnt, const double* sval,
-                                    const int32_t* sdep, const int8_t* sown, FoldStack* out,
+                                    const uint64_t* sid, const int8_t* sown, FoldStack* out,
                                     int32_t* flags, cudaStream_t st) {
     const int64_t ng = (hi - lo + G - 1) / G;
     const unsigned grid = (unsigned)((ng + 127) / 128);
-    sigma_merge_rows_kernel<<<grid, 128, 0, st>>>(n, lo, hi, G, row_vals, row_deps, row_cnt, sval,
-                                                  sdep, sown, out, flags);
+    sigma_merge_rows_kernel<<<grid, 128, 0, st>>>(n, lo, hi, G, row_vals, row_ids, row_cnt, sval,
+                                                  sid, sown, out, flags);
     return cudaGetLastError();
 }
 

@@ -10,14 +10,14 @@ struct FoldStack;
 // exact_passes.cu
 size_t sigma_rowstack_entries(int64_t rows);
 cudaError_t launch_sigma_pass(const double* X, int64_t n, int d, int64_t lo, int64_t hi, int want_p,
-                              double* row_vals, int32_t* row_deps, int32_t* row_cnt, int32_t* flags,
+                              double* row_vals, uint64_t* row_ids, int32_t* row_cnt, int32_t* flags,
                               int32_t* nn_j, double* nn_d, int8_t* nn_tie, double* pfold,
                               cudaStream_t st);
 cudaError_t launch_sigma_straddle(const double* X, int64_t n, int d, int64_t b_lo, int64_t b_hi,
-                                  double* sval, int32_t* sdep, int8_t* sown, cudaStream_t st);
+                                  double* sval, uint64_t* sid, int8_t* sown, cudaStream_t st);
 cudaError_t launch_sigma_merge_rows(int64_t n, int64_t lo, int64_t hi, int G, const double* row_vals,
-                                    const int32_t* row_deps, const int32_t* row_cnt,
-                                    const double* sval, const int32_t* sdep, const int8_t* sown,
+                                    const uint64_t* row_ids, const int32_t* row_cnt,
+                                    const double* sval, const uint64_t* sid, const int8_t* sown,
                                     FoldStack* out, int32_t* flags, cudaStream_t st);
 cudaError_t launch_stack_merge(const FoldStack* in, int64_t nin, int G, FoldStack* out,
                                int32_t* flags, cudaStream_t st);
