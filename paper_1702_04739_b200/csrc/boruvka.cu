@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace isoc {
 
@@ -436,6 +437,7 @@ cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, double* 
     prep_fp32_kernel<<<blocks_for(n, 256), 256, 0, st>>>(X, centre, n, d, dp, Y, ny, rad);
     cudaMemsetAsync(rmax_bits, 0, sizeof(uint32_t), st);
     max_float_kernel<<<296, 256, 0, st>>>(rad, n, rmax_bits);
+    note_launch(3);
     return cudaGetLastError();
 }
 
@@ -447,8 +449,11 @@ cudaError_t launch_boruvka_filter(const float* Y, const float* ny, const int32_t
     cudaError_t e = cudaFuncSetAttribute(boruvka_filter_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    const int pid = prof_begin(PK_FILTER, st);
     boruvka_filter_kernel<<<blocks_for(hi - lo, FM), FT, smem, st>>>(Y, ny, comp, n, dp, lo, hi, a1,
                                                                        j1, a2);
+    prof_end(pid, st);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -468,8 +473,11 @@ cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float
     candidate_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(X, d, a1, j1, a2, rad, comp, lo, hi,
                                                              rmax_bits, cd, compB, cand_d, cand_j,
                                                              cand_state, rescan_list, rescan_count);
+    const int pid = prof_begin(PK_RESCAN, st);
     rescan_kernel<<<592, 256, 0, st>>>(X, n, d, comp, lo, rescan_list, rescan_count, cand_d, cand_j,
                                        cand_tie);
+    prof_end(pid, st);
+    note_launch(3);
     return cudaGetLastError();
 }
 
@@ -479,6 +487,7 @@ cudaError_t launch_nn_candidates(const int32_t* nn_j, const double* nn_d, const 
     if (rows <= 0) return cudaSuccess;
     nn_candidates_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(nn_j, nn_d, nn_tie, rows, cand_d,
                                                                  cand_j, cand_state, cand_tie);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -489,6 +498,7 @@ cudaError_t launch_comp_exact_min(const double* cand_d, const int8_t* cand_state
     if (hi > lo)
         comp_exact_min_kernel<<<blocks_for(hi - lo, 256), 256, 0, st>>>(cand_d, cand_state, comp, lo,
                                                                          hi, compD);
+    note_launch(2);
     return cudaGetLastError();
 }
 
@@ -500,6 +510,7 @@ cudaError_t launch_comp_edge(const double* cand_d, const int32_t* cand_j, const 
     if (hi > lo)
         comp_edge_kernel<<<blocks_for(hi - lo, 256), 256, 0, st>>>(cand_d, cand_j, cand_state, comp,
                                                                     lo, hi, compD, compE);
+    note_launch(2);
     return cudaGetLastError();
 }
 
@@ -511,6 +522,7 @@ cudaError_t launch_comp_ties(const double* cand_d, const int32_t* cand_j, const 
         comp_tie_kernel<<<blocks_for(hi - lo, 256), 256, 0, st>>>(cand_d, cand_j, cand_state,
                                                                    cand_tie, comp, lo, hi, compD,
                                                                    compE, ties);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -528,6 +540,7 @@ cudaError_t launch_hook_contract(int32_t* comp, int64_t n, const unsigned long l
     for (int p = 0; p < passes + 1; ++p) jump_kernel<<<g, 256, 0, st>>>(comp, n, succ2, changed);
     cudaMemsetAsync(nroots, 0, sizeof(int32_t), st);
     relabel_kernel<<<g, 256, 0, st>>>(comp, n, succ2, nroots);
+    note_launch(passes + 4);
     return cudaGetLastError();
 }
 

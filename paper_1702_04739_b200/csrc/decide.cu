@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace isoc {
 
@@ -186,7 +187,11 @@ cudaError_t launch_decide(int64_t n, int64_t levels, const int64_t* level_off, i
     A.bar = reinterpret_cast<unsigned int*>(scratch + 1024);
     cudaMemsetAsync(A.bar, 0, 2 * sizeof(unsigned int), st);
     void* args[] = {&A};
-    return cudaLaunchCooperativeKernel((void*)decide_kernel, dim3(G), dim3(512), args, 0, st);
+    const int pid = prof_begin(PK_DECIDE, st);
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)decide_kernel, dim3(G), dim3(512), args, 0, st);
+    prof_end(pid, st);
+    note_launch();
+    return e;
 }
 
 // ----------------------------------------------------------------- labels
@@ -257,6 +262,7 @@ cudaError_t launch_labels(const int8_t* code, const int32_t* pos_parent, const i
     cub::DeviceScan::ExclusiveSum(tmp, tb, cut_i, scan, (int)n, st);
     cudaFreeAsync(tmp, st);
     labels_kernel<<<nb(n, 256), 256, 0, st>>>(rep, code, bfs, scan, n, eta, labels, lab32);
+    note_launch(passes + 3);
     return cudaGetLastError();
 }
 
@@ -447,6 +453,7 @@ cudaError_t launch_cost(const int32_t* lab32, const int32_t* parent_v, const dou
     segment_sum_kernel<<<(unsigned)(3 * k), 256, 0, st>>>(bvals_s, mvals_s, omega, p, bseg, mseg,
                                                           slot_off, svals, sflags, sums);
     miso_kernel<<<1, 1, 0, st>>>(sums, k, miso);
+    note_launch(6);
     return cudaGetLastError();
 }
 

@@ -3,16 +3,19 @@
 //
 //  K1 sigma_pass: distances bit-identical to scipy cdist (affinity.py:124-158),
 //     folded into numpy's pairwise_sum over the flat row-major n*n buffer
-//     (auto_sigma, affinity.py:233-241).  Each CTA owns a block of rows and
-//     streams 128-column tiles through a 256-column shared-memory ring; each
-//     recursion leaf (<=128 flat elements) that lies inside one row is summed
-//     from the ring with numpy's 8-accumulator kernel and pushed onto a per-row
-//     stack of maximal complete recursion nodes.  Leaves that cross a row
-//     boundary are summed by sigma_straddle_kernel; sigma_merge_kernel
-//     concatenates the row stacks in flat order, which folds them into the
-//     exact recursion tree.  The same pass also yields the exact nearest
-//     neighbour of every row (Boruvka round 1) and, when alpha > 0, the
-//     pow2 row folds of d for the potentials (affinity.py:204-230).
+//     (auto_sigma, affinity.py:233-241).  Each CTA owns 32 rows and streams
+//     128-column tiles of the transposed points through a cp.async double
+//     buffer.  Recursion leaves start at multiples of 8 and (except the very
+//     last leaf) have lengths that are multiples of 8, so numpy's 8-way leaf
+//     kernel is an "octet" stream: lane j of an 8-lane group accumulates the
+//     flat elements = j (mod 8) of its row; at a leaf end the group combines
+//     ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and pushes the value onto the row's
+//     stack of complete recursion nodes.  A 7-element carry bridges octets
+//     split across tiles.  Leaves crossing a row boundary are summed by
+//     sigma_straddle_kernel; merge kernels push the row stacks in flat order,
+//     which folds the exact recursion tree.  The same pass yields the exact
+//     nearest neighbour of every row (Boruvka round 1) and, when alpha > 0,
+//     the pow2 row folds of d (potentials, affinity.py:204-230).
 //  K2 omega_pass: omega_i = pow2 fold over j of exp(-d_ij/sigma), diagonal
 //     zeroed (affinity.py:175-201, _primitives.py:162-175).  128-column tiles
 //     are complete subtrees of the pow2 fold; a per-row binary counter folds
@@ -22,61 +25,121 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace isoc {
 
 constexpr int XM = 32;        // rows per CTA
 constexpr int XN = 128;       // columns per tile
 constexpr int XK = 16;        // k chunk
-constexpr int XT = 256;       // threads
-constexpr int RING = 256;     // ring columns (two tiles)
+constexpr int XTH = 256;      // threads
 constexpr int ROW_CAP = 40;   // per-row stack capacity (<= 2 log2(n/64) + 2 used)
 constexpr int PC_LEVELS = 32; // binary-counter levels for pow2 row folds
 
-struct TileSmem {
-    double As[XK][XM];
-    double Bs[XK][XN + 1];
+// Transposed, zero-padded copy of the points: XT[k * np + i] = X[i, k] for
+// k < dpad (multiple of XK), i < np (multiple of XN).
+__global__ void transpose_pad_kernel(const double* __restrict__ X, int64_t n, int d, int64_t np,
+                                     int dpad, double* __restrict__ XT) {
+    __shared__ double t[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    const int k0 = blockIdx.y * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int64_t i = i0 + y;
+        const int k = k0 + threadIdx.x;
+        t[y][threadIdx.x] = (i < n && k < d) ? X[i * d + k] : 0.0;
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int k = k0 + y;
+        const int64_t i = i0 + threadIdx.x;
+        if (k < dpad && i < np) XT[(int64_t)k * np + i] = t[threadIdx.x][y];
+    }
+}
+
+struct Stage {
+    double A[XK][XM];
+    double B[XK][XN];
 };
 
-// Accumulate the exact squared distances of rows [r0, r0+XM) x cols
-// [c0, c0+XN) into acc (thread owns rows ty+8i, cols tx+32j).
-__device__ __forceinline__ void exact_tile(const double* __restrict__ X, int64_t n, int d,
-                                           int64_t r0, int64_t c0, TileSmem& sm,
-                                           double acc[4][4]) {
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Issue the cp.async copies of k-chunk kc for rows [r0, r0+32) and columns
+// [c0, c0+128) from XT (row stride np).
+__device__ __forceinline__ void load_stage(Stage& s, const double* __restrict__ XT, int64_t np,
+                                           int64_t r0, int64_t c0, int kc) {
     const int tid = threadIdx.x;
-    const int tx = tid & 31, ty = tid >> 5;
+    // rows: 8-byte copies (a shard's first row may be odd)
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int m = 0; m < 2; ++m) {
+        const int q = tid + XTH * m;
+        const int kk = q >> 5, r = q & 31;
+        cp_async8(&s.A[kk][r], XT + (int64_t)(kc * XK + kk) * np + r0 + r);
+    }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    for (int k0 = 0; k0 < d; k0 += XK) {
-        __syncthreads();
-        // rows: 32 x 16
-        for (int e = tid; e < XM * XK; e += XT) {
-            int r = e / XK, kk = e % XK;
-            int64_t row = r0 + r;
-            int k = k0 + kk;
-            sm.As[kk][r] = (row < n && k < d) ? X[row * d + k] : 0.0;
-        }
-        for (int e = tid; e < XN * XK; e += XT) {
-            int c = e / XK, kk = e % XK;
-            int64_t col = c0 + c;
-            int k = k0 + kk;
-            sm.Bs[kk][c] = (col < n && k < d) ? X[col * d + k] : 0.0;
-        }
-        __syncthreads();
-        const int kmax = (d - k0) < XK ? (d - k0) : XK;
-        for (int kk = 0; kk < kmax; ++kk) {
-            double a[4], b[4];
+    for (int m = 0; m < 4; ++m) {
+        const int q = tid + XTH * m;
+        const int kk = q >> 6, part = q & 63;
+        cp_async16(&s.B[kk][part * 2], XT + (int64_t)(kc * XK + kk) * np + c0 + part * 2);
+    }
+}
+
+__device__ __forceinline__ void compute_stage(const Stage& s, double acc[4][4]) {
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = sm.As[kk][ty + 8 * i];
+    for (int kk = 0; kk < XK; ++kk) {
+        double a[4], b[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = sm.Bs[kk][tx + 32 * j];
+        for (int i = 0; i < 4; ++i) a[i] = s.A[kk][ty + 8 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = s.B[kk][tx + 32 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = exact_sq_step(acc[i][j], a[i], b[j]);
+    }
+}
+
+// Software pipeline over (tile, k-chunk): the epilogue of tile t runs while
+// the first chunk of tile t+1 is in flight.  `epi(t, acc)` must end with all
+// threads done reading shared state it shares with the next epilogue.
+template <typename Epi>
+__device__ __forceinline__ void exact_tiles(const double* __restrict__ XT, int64_t np, int dpad,
+                                            int64_t r0, int64_t ntiles, Stage* st, Epi epi) {
+    const int nk = dpad / XK;
+    const int64_t total = ntiles * nk;
+    double acc[4][4];
+    load_stage(st[0], XT, np, r0, 0, 0);
+    cp_commit();
+    for (int64_t it = 0; it < total; ++it) {
+        const int64_t t = it / nk;
+        const int kc = (int)(it % nk);
+        if (kc == 0) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = exact_sq_step(acc[i][j], a[i], b[j]);
+                for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
         }
+        if (it + 1 < total) {
+            const int64_t t1 = (it + 1) / nk;
+            const int kc1 = (int)((it + 1) % nk);
+            load_stage(st[(it + 1) & 1], XT, np, r0, t1 * XN, kc1);
+        }
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        compute_stage(st[it & 1], acc);
+        __syncthreads();
+        if (kc == nk - 1) epi(t, acc);
     }
 }
 
@@ -134,193 +197,180 @@ __device__ __forceinline__ NNState nn_combine(NNState a, NNState b) {
     return f;
 }
 
+// per-thread running (m1, j1, m2) with columns visited in increasing order
+__device__ __forceinline__ void nn_update(NNState& s, double v, int64_t j) {
+    if (v < s.m1) {
+        s.m2 = s.m1;
+        s.m1 = v;
+        s.j1 = j;
+    } else {
+        s.m2 = fmin(s.m2, v);
+    }
+}
+
 // --------------------------------------------------------------- K1
 struct SigmaSmem {
-    TileSmem tile;
-    double ring[XM][RING];
+    Stage st[2];
+    double D[XM][XN];
     double st_val[XM][ROW_CAP];
     uint64_t st_id[XM][ROW_CAP];
+    double carry[XM][8];
     double pc[XM][PC_LEVELS];
-    int64_t lf_start[XM];
-    int32_t lf_len[XM];
-    uint64_t lf_id[XM];
-    int32_t lf_done[XM];
     int32_t st_cnt[XM];
     int32_t st_ovf[XM];
 };
 
-__global__ void __launch_bounds__(XT, 2)
-sigma_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo, int64_t row_hi,
-                  int want_p, double* __restrict__ row_vals, uint64_t* __restrict__ row_ids,
-                  int32_t* __restrict__ row_cnt, int32_t* __restrict__ flags,
-                  int32_t* __restrict__ nn_j, double* __restrict__ nn_d, int8_t* __restrict__ nn_tie,
-                  double* __restrict__ pfold) {
+__global__ void __launch_bounds__(XTH, 2)
+sigma_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n, int64_t row_lo,
+                  int64_t row_hi, int want_p, double* __restrict__ row_vals,
+                  uint64_t* __restrict__ row_ids, int32_t* __restrict__ row_cnt,
+                  int32_t* __restrict__ flags, int32_t* __restrict__ nn_j, double* __restrict__ nn_d,
+                  int8_t* __restrict__ nn_tie, double* __restrict__ pfold) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SigmaSmem& sm = *reinterpret_cast<SigmaSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tx = lane, ty = warp;
     const int64_t r0 = row_lo + (int64_t)blockIdx.x * XM;
     const int64_t total = n * n;
 
+    // octet-stream state: group g of warp w owns row w + 8g; lane j8 owns
+    // accumulator j8.  [s_first, e_last) = internal (non-straddling) leaves.
+    const int g = lane >> 3, j8 = lane & 7;
+    const int orow = warp + 8 * g;
+    const int64_t grow = r0 + orow;
+    const int64_t rs = grow * n, re = rs + n;
+    int64_t s_first = re, e_last = re, leaf_end = 0;
+    uint64_t leaf_id = 0;
+    if (grow < row_hi) {
+        Leaf L = find_leaf(total, rs);
+        if (L.start < rs) L = (L.start + L.len < re) ? find_leaf(total, L.start + L.len) : Leaf{re, 0, 0};
+        if (L.len > 0 && L.start + L.len <= re) {
+            s_first = L.start;
+            leaf_end = L.start + L.len;
+            leaf_id = L.hid;
+            // the octet stream covers leaves inside the row whose length is a
+            // multiple of 8: the row's last leaf is excluded when it straddles
+            // into the next row or is the global final leaf with a tail
+            // (total % 8 != 0); the straddle kernel sums those.
+            Leaf E = find_leaf(total, re - 1);
+            const bool final_tail = (E.start + E.len == total) && (total % 8 != 0);
+            e_last = (E.start + E.len <= re && !final_tail) ? re : E.start;
+        }
+    }
+    double acc8 = 0.0;
     if (tid < XM) {
-        int64_t row = r0 + tid;
         sm.st_cnt[tid] = 0;
         sm.st_ovf[tid] = 0;
-        int done = 1;
-        if (row < row_hi) {
-            int64_t rs = row * n, re = rs + n;
-            Leaf L = find_leaf(total, rs);
-            if (L.start < rs) L = (L.start + L.len < re) ? find_leaf(total, L.start + L.len) : Leaf{re, 0, 0};
-            if (L.len > 0 && L.start + L.len <= re) {
-                done = 0;
-                sm.lf_start[tid] = L.start;
-                sm.lf_len[tid] = (int32_t)L.len;
-                sm.lf_id[tid] = L.hid;
-            }
-        }
-        sm.lf_done[tid] = done;
     }
+
     NNState nn[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) nn[q] = NNState{INFINITY, INFINITY, -1};
+    for (int i = 0; i < 4; ++i) nn[i] = NNState{INFINITY, INFINITY, -1};
 
     const int64_t ntiles = (n + XN - 1) / XN;
-    for (int64_t t = 0; t < ntiles; ++t) {
+    exact_tiles(XT, np, dpad, r0, ntiles, sm.st, [&](int64_t t, double (&acc)[4][4]) {
         const int64_t c0 = t * XN;
-        double acc[4][4];
-        exact_tile(X, n, d, r0, c0, sm.tile, acc);
-        const int tx = tid & 31, ty = tid >> 5;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i) {
+            const int64_t row = r0 + ty + 8 * i;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                int64_t col = c0 + tx + 32 * j;
-                sm.ring[ty + 8 * i][(col) & (RING - 1)] = col < n ? __dsqrt_rn(acc[i][j]) : 0.0;
+                const int64_t col = c0 + tx + 32 * j;
+                const double v = __dsqrt_rn(acc[i][j]);
+                sm.D[ty + 8 * i][tx + 32 * j] = col < n ? v : 0.0;
+                if (col < n && col != row) nn_update(nn[i], v, col);
             }
-        __syncthreads();
-
-        // nearest neighbour (exact, ties -> smaller column) for 4 rows per warp
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int r = warp + 8 * q;
-            const int64_t row = r0 + r;
-            NNState s{INFINITY, INFINITY, -1};
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                int64_t col = c0 + lane + 32 * m;
-                if (col < n && col != row) {
-                    double v = sm.ring[r][col & (RING - 1)];
-                    s = nn_combine(s, NNState{v, INFINITY, col});
-                }
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                NNState o;
-                o.m1 = __shfl_xor_sync(0xffffffffu, s.m1, off);
-                o.m2 = __shfl_xor_sync(0xffffffffu, s.m2, off);
-                o.j1 = __shfl_xor_sync(0xffffffffu, s.j1, off);
-                s = nn_combine(s, o);
-            }
-            nn[q] = nn_combine(nn[q], s);
         }
-
-        // pow2 row folds of d for potentials
+        __syncthreads();
         if (want_p) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int r = warp + 8 * q;
-                double s = warp_fold128([&](int c) { return sm.ring[r][(c0 + c) & (RING - 1)]; });
+                double s = warp_fold128([&](int c) { return sm.D[r][c]; });
                 if (lane == 0) counter_push(sm.pc[r], t, s);
             }
         }
-
-        // sigma leaves ending inside this tile: 8 lanes per row, 4 rows per warp
-        {
-            const int g = lane >> 3, j8 = lane & 7;
-            const int r = warp + 8 * g;
-            const int64_t row = r0 + r;
-            const int64_t rs = row * n, re = rs + n;
-            const unsigned gmask = 0xffu << (8 * g);
-            while (true) {
-                int active = !sm.lf_done[r] &&
-                             (sm.lf_start[r] + sm.lf_len[r] - rs) <= c0 + XN;
-                if (!__any_sync(0xffffffffu, active)) break;
-                double res = 0.0;
-                if (active) {
-                    const int64_t ls = sm.lf_start[r] - rs;  // row-relative start
-                    const int len = sm.lf_len[r];
-                    const int main_end = len - (len % 8);
-                    double acc8 = 0.0;
-                    if (len >= 8) {
-                        acc8 = sm.ring[r][(ls + j8) & (RING - 1)];
-                        for (int i = 8; i < main_end; i += 8)
-                            acc8 = __dadd_rn(acc8, sm.ring[r][(ls + i + j8) & (RING - 1)]);
-                    }
-                    double o = __shfl_down_sync(gmask, acc8, 1);
-                    if ((j8 & 1) == 0) acc8 = __dadd_rn(acc8, o);
-                    o = __shfl_down_sync(gmask, acc8, 2);
-                    if ((j8 & 3) == 0) acc8 = __dadd_rn(acc8, o);
-                    o = __shfl_down_sync(gmask, acc8, 4);
-                    if (j8 == 0) {
-                        if (len >= 8) {
-                            res = __dadd_rn(acc8, o);
-                            for (int i = main_end; i < len; ++i)
-                                res = __dadd_rn(res, sm.ring[r][(ls + i) & (RING - 1)]);
-                        } else {
-                            res = 0.0;
-                            for (int i = 0; i < len; ++i)
-                                res = __dadd_rn(res, sm.ring[r][(ls + i) & (RING - 1)]);
-                        }
-                        int cnt = sm.st_cnt[r], ovf = sm.st_ovf[r];
-                        stack_push(sm.st_val[r], sm.st_id[r], cnt, ROW_CAP, ovf, res, sm.lf_id[r]);
-                        sm.st_cnt[r] = cnt;
-                        sm.st_ovf[r] = ovf;
-                        int64_t end = sm.lf_start[r] + sm.lf_len[r];
-                        if (end >= re) {
-                            sm.lf_done[r] = 1;
-                        } else {
-                            Leaf L = find_leaf(total, end);
-                            if (L.start + L.len > re) {
-                                sm.lf_done[r] = 1;
-                            } else {
-                                sm.lf_start[r] = L.start;
-                                sm.lf_len[r] = (int32_t)L.len;
-                                sm.lf_id[r] = L.hid;
-                            }
-                        }
+        // octets of row `orow` that complete inside this tile
+        const int64_t tf0 = rs + c0;                              // first flat index of the tile
+        const int64_t tf1 = rs + ((c0 + XN < n) ? c0 + XN : n);   // one past the last
+        // octet o completes here iff 8o+8 in (tf0, tf1]
+        const int64_t o_first = ((tf0 >> 3) > (s_first >> 3)) ? (tf0 >> 3) : (s_first >> 3);
+        const int64_t o_end_excl = ((tf1 < e_last ? tf1 : e_last) >> 3);
+        for (int q = 0; q < XN / 8 + 2; ++q) {
+            const int64_t o = o_first + q;
+            const bool active = (grow < row_hi) && o < o_end_excl && (8 * o + 8 > tf0);
+            if (!__any_sync(0xffffffffu, active)) break;
+            if (active) {
+                const int64_t f = 8 * o + j8;
+                const double v = (f < tf0) ? sm.carry[orow][j8] : sm.D[orow][f - rs - c0];
+                acc8 = __dadd_rn(acc8, v);
+            }
+            const bool ending = active && (8 * o + 8 == leaf_end);
+            if (__any_sync(0xffffffffu, ending)) {
+                double x = acc8;
+                double y = __shfl_down_sync(0xffffffffu, x, 1);
+                if ((j8 & 1) == 0) x = __dadd_rn(x, y);
+                y = __shfl_down_sync(0xffffffffu, x, 2);
+                if ((j8 & 3) == 0) x = __dadd_rn(x, y);
+                y = __shfl_down_sync(0xffffffffu, x, 4);
+                if (ending && j8 == 0) {
+                    x = __dadd_rn(x, y);
+                    int cnt = sm.st_cnt[orow], ovf = sm.st_ovf[orow];
+                    stack_push(sm.st_val[orow], sm.st_id[orow], cnt, ROW_CAP, ovf, x, leaf_id);
+                    sm.st_cnt[orow] = cnt;
+                    sm.st_ovf[orow] = ovf;
+                    if (leaf_end < e_last) {
+                        Leaf L = find_leaf(total, leaf_end);
+                        leaf_end = L.start + L.len;
+                        leaf_id = L.hid;
                     }
                 }
-                __syncwarp();
+                if (ending) acc8 = 0.0;
+                leaf_end = __shfl_sync(0xffffffffu, leaf_end, lane & ~7);
+                leaf_id = __shfl_sync(0xffffffffu, leaf_id, lane & ~7);
             }
+        }
+        // carry the partial octet at the tile end
+        {
+            const int64_t f = (tf1 & ~int64_t(7)) + j8;
+            if (grow < row_hi && f < tf1 && f >= tf0) sm.carry[orow][j8] = sm.D[orow][f - rs - c0];
         }
         __syncthreads();
-    }
+    });
 
-    // outputs
-    if (lane == 0) {
+    // nearest neighbours: reduce the 32 column lanes of each row
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int r = warp + 8 * q;
-            const int64_t row = r0 + r;
-            if (row < row_hi) {
-                int64_t li = row - row_lo;
-                nn_j[li] = (int32_t)nn[q].j1;
-                nn_d[li] = nn[q].m1;
-                nn_tie[li] = (int8_t)(nn[q].m2 == nn[q].m1);
-                if (want_p) pfold[li] = counter_flush(sm.pc[r], ntiles);
-            }
+    for (int i = 0; i < 4; ++i) {
+        NNState s = nn[i];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            NNState o;
+            o.m1 = __shfl_xor_sync(0xffffffffu, s.m1, off);
+            o.m2 = __shfl_xor_sync(0xffffffffu, s.m2, off);
+            o.j1 = __shfl_xor_sync(0xffffffffu, s.j1, off);
+            s = nn_combine(s, o);
+        }
+        const int64_t row = r0 + ty + 8 * i;
+        if (lane == 0 && row < row_hi) {
+            const int64_t li = row - row_lo;
+            nn_j[li] = (int32_t)s.j1;
+            nn_d[li] = s.m1;
+            nn_tie[li] = (int8_t)(s.m2 == s.m1);
+            if (want_p) pfold[li] = counter_flush(sm.pc[ty + 8 * i], ntiles);
         }
     }
-    for (int e = tid; e < XM * ROW_CAP; e += XT) {
-        int r = e / ROW_CAP, s = e % ROW_CAP;
-        int64_t row = r0 + r;
+    __syncthreads();
+    for (int e = tid; e < XM * ROW_CAP; e += XTH) {
+        const int r = e / ROW_CAP, s = e % ROW_CAP;
+        const int64_t row = r0 + r;
         if (row < row_hi && s < sm.st_cnt[r]) {
-            int64_t li = row - row_lo;
+            const int64_t li = row - row_lo;
             row_vals[li * ROW_CAP + s] = sm.st_val[r][s];
             row_ids[li * ROW_CAP + s] = sm.st_id[r][s];
         }
     }
     if (tid < XM) {
-        int64_t row = r0 + tid;
+        const int64_t row = r0 + tid;
         if (row < row_hi) {
             row_cnt[row - row_lo] = sm.st_cnt[tid];
             if (sm.st_ovf[tid]) atomicOr(flags, 1);
@@ -338,13 +388,21 @@ __global__ void sigma_straddle_kernel(const double* __restrict__ X, int64_t n, i
     const int64_t b = b_lo + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (b >= b_hi) return;
     const int64_t total = n * n;
-    Leaf L = find_leaf(total, b * n);
-    const bool own = (L.start < b * n) && (L.start / n == b - 1);
+    Leaf L;
+    bool own;
+    if (b < n) {
+        L = find_leaf(total, b * n);
+        own = (L.start < b * n) && (L.start / n == b - 1);
+    } else {
+        // boundary n: the final leaf, when it has a tail (total % 8 != 0) and
+        // lies inside the last row (otherwise an earlier boundary owns it)
+        L = find_leaf(total, total - 1);
+        own = (total % 8 != 0) && (L.start >= (n - 1) * n);
+    }
     if (!own) {
         if (lane == 0) sown[b - b_lo] = 0;
         return;
     }
-    // distances of the leaf elements: lane handles elements lane + 32m
     double v[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -366,7 +424,6 @@ __global__ void sigma_straddle_kernel(const double* __restrict__ X, int64_t n, i
         }
         return r;
     };
-    // all lanes walk the same sequential leaf kernel (uniform control flow)
     double res = np_leaf_sum(get, L.len);
     if (lane == 0) {
         sval[b - b_lo] = res;
@@ -377,7 +434,7 @@ __global__ void sigma_straddle_kernel(const double* __restrict__ X, int64_t n, i
 
 // Merge level 1: rows [lo, hi) in groups of G rows -> one FoldStack each.
 // Sequence per row i: straddle(i) if i > lo and owned, then row stack(i);
-// the last group also appends straddle(hi) (hi < n).
+// the last group also appends straddle(hi) (boundary n = the final leaf).
 __global__ void sigma_merge_rows_kernel(int64_t n, int64_t lo, int64_t hi, int G,
                                         const double* __restrict__ row_vals,
                                         const uint64_t* __restrict__ row_ids,
@@ -401,7 +458,7 @@ __global__ void sigma_merge_rows_kernel(int64_t n, int64_t lo, int64_t hi, int G
             stack_push(S.value, S.id, cnt, kStackCap, ovf, row_vals[li * ROW_CAP + s],
                        row_ids[li * ROW_CAP + s]);
     }
-    if (b == hi && hi < n && sown[hi - lo - 1])
+    if (b == hi && sown[hi - lo - 1])
         stack_push(S.value, S.id, cnt, kStackCap, ovf, sval[hi - lo - 1], sid[hi - lo - 1]);
     S.count = cnt;
     S.overflow = ovf;
@@ -429,24 +486,22 @@ __global__ void stack_merge_kernel(const FoldStack* __restrict__ in, int64_t nin
 
 // --------------------------------------------------------------- K2
 struct OmegaSmem {
-    TileSmem tile;
+    Stage st[2];
     double D[XM][XN];
     double pc[XM][PC_LEVELS];
 };
 
-__global__ void __launch_bounds__(XT, 2)
-omega_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo,
+__global__ void __launch_bounds__(XTH, 2)
+omega_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n, int64_t row_lo,
                   int64_t row_hi, double sigma, double* __restrict__ omega) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     OmegaSmem& sm = *reinterpret_cast<OmegaSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tx = tid & 31, ty = tid >> 5;
+    const int tx = lane, ty = warp;
     const int64_t r0 = row_lo + (int64_t)blockIdx.x * XM;
     const int64_t ntiles = (n + XN - 1) / XN;
-    for (int64_t t = 0; t < ntiles; ++t) {
+    exact_tiles(XT, np, dpad, r0, ntiles, sm.st, [&](int64_t t, double (&acc)[4][4]) {
         const int64_t c0 = t * XN;
-        double acc[4][4];
-        exact_tile(X, n, d, r0, c0, sm.tile, acc);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -464,8 +519,8 @@ omega_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo
             double s = warp_fold128([&](int c) { return sm.D[r][c]; });
             if (lane == 0) counter_push(sm.pc[r], t, s);
         }
-    }
-    __syncthreads();
+        __syncthreads();
+    });
     if (lane == 0) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -479,19 +534,39 @@ omega_pass_kernel(const double* __restrict__ X, int64_t n, int d, int64_t row_lo
 // ----------------------------------------------------------- launchers
 size_t sigma_rowstack_entries(int64_t rows) { return (size_t)rows * ROW_CAP; }
 
+static cudaError_t make_xt(const double* X, int64_t n, int d, double** XT, int64_t* np, int* dpad,
+                           cudaStream_t st) {
+    *np = (n + XN - 1) / XN * XN + XN;
+    *dpad = (d + XK - 1) / XK * XK;
+    cudaError_t e = cudaMallocAsync((void**)XT, (size_t)(*np) * (*dpad) * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((*np + 31) / 32), (unsigned)((*dpad + 31) / 32));
+    transpose_pad_kernel<<<grid, dim3(32, 8), 0, st>>>(X, n, d, *np, *dpad, *XT);
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sigma_pass(const double* X, int64_t n, int d, int64_t lo, int64_t hi,
                               int want_p, double* row_vals, uint64_t* row_ids, int32_t* row_cnt,
                               int32_t* flags, int32_t* nn_j, double* nn_d, int8_t* nn_tie,
                               double* pfold, cudaStream_t st) {
     const int64_t rows = hi - lo;
     if (rows <= 0) return cudaSuccess;
+    double* XT = nullptr;
+    int64_t np = 0;
+    int dpad = 0;
+    cudaError_t e = make_xt(X, n, d, &XT, &np, &dpad, st);
+    if (e != cudaSuccess) return e;
     const size_t smem = sizeof(SigmaSmem);
-    cudaError_t e = cudaFuncSetAttribute(sigma_pass_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(sigma_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((rows + XM - 1) / XM);
-    sigma_pass_kernel<<<grid, XT, smem, st>>>(X, n, d, lo, hi, want_p, row_vals, row_ids, row_cnt,
-                                              flags, nn_j, nn_d, nn_tie, pfold);
+    const int pid = prof_begin(PK_SIGMA, st);
+    sigma_pass_kernel<<<grid, XTH, smem, st>>>(XT, np, dpad, n, lo, hi, want_p, row_vals, row_ids,
+                                              row_cnt, flags, nn_j, nn_d, nn_tie, pfold);
+    prof_end(pid, st);
+    note_launch();
+    cudaFreeAsync(XT, st);
     return cudaGetLastError();
 }
 
@@ -501,6 +576,7 @@ cudaError_t launch_sigma_straddle(const double* X, int64_t n, int d, int64_t b_l
     if (nb <= 0) return cudaSuccess;
     const unsigned grid = (unsigned)((nb * 32 + 255) / 256);
     sigma_straddle_kernel<<<grid, 256, 0, st>>>(X, n, d, b_lo, b_hi, sval, sid, sown);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -513,6 +589,7 @@ cudaError_t launch_sigma_merge_rows(int64_t n, int64_t lo, int64_t hi, int G,
     const unsigned grid = (unsigned)((ng + 127) / 128);
     sigma_merge_rows_kernel<<<grid, 128, 0, st>>>(n, lo, hi, G, row_vals, row_ids, row_cnt, sval,
                                                   sid, sown, out, flags);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -521,6 +598,7 @@ cudaError_t launch_stack_merge(const FoldStack* in, int64_t nin, int G, FoldStac
     const int64_t nout = (nin + G - 1) / G;
     const unsigned grid = (unsigned)((nout + 127) / 128);
     stack_merge_kernel<<<grid, 128, 0, st>>>(in, nin, G, out, flags);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -528,12 +606,20 @@ cudaError_t launch_omega_pass(const double* X, int64_t n, int d, int64_t lo, int
                               double sigma, double* omega, cudaStream_t st) {
     const int64_t rows = hi - lo;
     if (rows <= 0) return cudaSuccess;
+    double* XT = nullptr;
+    int64_t np = 0;
+    int dpad = 0;
+    cudaError_t e = make_xt(X, n, d, &XT, &np, &dpad, st);
+    if (e != cudaSuccess) return e;
     const size_t smem = sizeof(OmegaSmem);
-    cudaError_t e = cudaFuncSetAttribute(omega_pass_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(omega_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((rows + XM - 1) / XM);
-    omega_pass_kernel<<<grid, XT, smem, st>>>(X, n, d, lo, hi, sigma, omega);
+    const int pid = prof_begin(PK_OMEGA, st);
+    omega_pass_kernel<<<grid, XTH, smem, st>>>(XT, np, dpad, n, lo, hi, sigma, omega);
+    prof_end(pid, st);
+    note_launch();
+    cudaFreeAsync(XT, st);
     return cudaGetLastError();
 }
 

@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace isoc {
 
@@ -358,6 +359,7 @@ cudaError_t launch_build_adjacency(const int32_t* eu, const int32_t* ev, const d
     cudaMemcpyAsync(deg, off, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
     if (m > 0) fill_adj_kernel<<<nblk(m, 256), 256, 0, st>>>(eu, ev, ed, m, deg, adj, adjd);
     sort_adj_kernel<<<nblk(n, 256), 256, 0, st>>>(off, n, adj, adjd);
+    note_launch(3);
     return cudaGetLastError();
 }
 
@@ -392,6 +394,7 @@ cudaError_t launch_children_from_parent(const int64_t* parent, const int64_t* ch
     cub::DeviceScan::ExclusiveSum(tmp, tb, deg, off, (int)(n + 1), st);
     cudaFreeAsync(tmp, st);
     child_ids_kernel<<<nblk(n, 256), 256, 0, st>>>(skeys, adj, off, n, child_id_v);
+    note_launch(3);
     cudaFreeAsync(keys, st); cudaFreeAsync(skeys, st); cudaFreeAsync(vals, st);
     cudaFreeAsync(pkeys, st); cudaFreeAsync(deg, st);
 #undef ACK
@@ -426,12 +429,17 @@ cudaError_t launch_bfs(int64_t n, int64_t root, int undirected, const int32_t* o
     A.out_levels = out_levels;
     cudaMemsetAsync(A.bar, 0, 2 * sizeof(unsigned int), st);
     void* args[] = {&A};
-    return cudaLaunchCooperativeKernel((void*)bfs_kernel, dim3(G), dim3(512), args, 0, st);
+    const int pid = prof_begin(PK_BFS, st);
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)bfs_kernel, dim3(G), dim3(512), args, 0, st);
+    prof_end(pid, st);
+    note_launch();
+    return e;
 }
 
 cudaError_t launch_flows(const double* parent_d, const int32_t* parent_v, int64_t n, double sigma,
                          double* flow, cudaStream_t st) {
     flows_kernel<<<nblk(n, 256), 256, 0, st>>>(parent_d, parent_v, n, sigma, flow);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -440,6 +448,7 @@ cudaError_t launch_gather_pos(const int32_t* bfs, int64_t n, const double* flow_
                               double* om_pos, double* p_pos, cudaStream_t st) {
     gather_pos_kernel<<<nblk(n, 256), 256, 0, st>>>(bfs, n, flow_v, omega_v, p_v, f_pos, om_pos,
                                                      p_pos);
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -447,6 +456,7 @@ cudaError_t launch_extrema(const double* flow_v, int64_t root, const double* ome
                            int64_t n, double* out6, double* tmp, unsigned long long* key,
                            cudaStream_t st) {
     // tmp: >= 2 * (next_pow2(n) / 2048 + 1) doubles
+    note_launch(12);
     pow2_sum<1>(flow_v, n - 1, root, out6 + 0, tmp, st);
     min_value<1>(flow_v, n - 1, root, out6 + 1, key, st);
     pow2_sum<0>(omega, n, 0, out6 + 2, tmp, st);

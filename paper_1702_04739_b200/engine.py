@@ -137,17 +137,23 @@ class CudaBackend:
         check(self.lib.isoc_mst_create(_ptr(X), n, d, lo, hi, self.stream, ctypes.byref(h)))
         return h
 
-    def mst_round(self, h, n: int, comm: Comm, nn=None):
-        torch = self.torch
-        cmin = self.empty((n,), torch.int64)
-        cedge = self.empty((n,), torch.int64)
+    def mst_round_local(self, h, n: int, nn=None):
+        """Local rows' per-component exact minimum weight keys (int64, n)."""
+        cmin = self.empty((n,), self.torch.int64)
         if nn is not None:
             check(self.lib.isoc_mst_round_local(h, 1, _ptr(nn[0]), _ptr(nn[1]), _ptr(nn[2]), _ptr(cmin)))
         else:
             check(self.lib.isoc_mst_round_local(h, 0, None, None, None, _ptr(cmin)))
-        comm.allreduce_min_(cmin)
+        return cmin
+
+    def mst_round_edges(self, h, cmin):
+        """Packed endpoint keys of local rows attaining the (global) minima."""
+        cedge = self.empty(tuple(cmin.shape), self.torch.int64)
         check(self.lib.isoc_mst_round_edges(h, _ptr(cmin), _ptr(cedge)))
-        comm.allreduce_min_(cedge)
+        return cedge
+
+    def mst_round_finish(self, h, cmin, cedge):
+        """Hook + contract with the global keys; (components, ties, rescans)."""
         comps, ties, rescans = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         check(self.lib.isoc_mst_round_finish(h, _ptr(cmin), _ptr(cedge), ctypes.byref(comps),
                                              ctypes.byref(ties), ctypes.byref(rescans)))

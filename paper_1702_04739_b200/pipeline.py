@@ -96,16 +96,41 @@ def _validate_k(k) -> None:
 
 
 # --------------------------------------------------------------- stages
+def _is_device_tensor(points) -> bool:
+    mod = type(points).__module__
+    return mod.startswith("torch") and getattr(points, "is_cuda", False)
+
+
 class _Points:
-    """Points resident on the device plus this rank's row shard."""
+    """Points resident on the device plus this rank's row shard.
+
+    Accepts host arrays (validated as affinity.py:70-81, then copied to HBM)
+    or a CUDA torch tensor already resident in HBM (same validation on the
+    device, no copy).
+    """
 
     def __init__(self, points, comm: Optional[Comm] = None, b: Optional[CudaBackend] = None):
         self.b = b or backend()
         self.comm = comm or Comm()
-        self.host = _validate_points(points)
-        self.n, self.d = self.host.shape
+        if _is_device_tensor(points):
+            torch = self.b.torch
+            X = points.to(torch.float64).contiguous()
+            if X.dim() != 2:
+                raise ValueError(f"points must be a 2-d array, got shape {tuple(X.shape)}")
+            n, d = X.shape
+            if n < 2:
+                raise ValueError(f"need at least 2 points, got {n}")
+            if d < 1:
+                raise ValueError("points must have at least one coordinate")
+            if not bool(torch.isfinite(X).all()):
+                raise ValueError("points must be finite")
+            self.host = None
+            self.X = X
+        else:
+            self.host = _validate_points(points)
+            self.X = self.b.to_device(self.host)
+        self.n, self.d = (int(v) for v in self.X.shape)
         self.lo, self.hi = self.comm.rows(self.n)
-        self.X = self.b.to_device(self.host)
 
 
 def _sigma_pass(P: _Points, alpha: float):
@@ -123,13 +148,23 @@ def _sigma_from_stack(P: _Points, stack) -> float:
 
 
 def _boruvka(P: _Points, nn=None) -> tuple:
-    """MST edges on the device; returns (u, v, w, stats)."""
+    """MST edges on the device; returns (u, v, w, stats).
+
+    Per round each rank reduces its row shard to per-component 64-bit keys;
+    two MIN all-reduces (weight bits, then packed endpoints of the rows that
+    attain the minimum) make the lexicographic (d, min, max) winner global,
+    after which hooking/contraction is replicated identically on every rank.
+    """
     b, comm, n = P.b, P.comm, P.n
     h = b.mst_create(P.X, n, P.d, P.lo, P.hi)
     try:
         comps, rounds, ties, rescans = n, 0, 0, 0
         while comps > 1:
-            c, t, r = b.mst_round(h, n, comm, nn if rounds == 0 else None)
+            cmin = b.mst_round_local(h, n, nn if rounds == 0 else None)
+            comm.allreduce_min_(cmin)
+            cedge = b.mst_round_edges(h, cmin)
+            comm.allreduce_min_(cedge)
+            c, t, r = b.mst_round_finish(h, cmin, cedge)
             rounds += 1
             ties += t
             rescans += r
@@ -142,7 +177,7 @@ def _boruvka(P: _Points, nn=None) -> tuple:
     if comm.world > 1:
         import torch
 
-        tt = torch.tensor([ties, rescans], dtype=torch.int64, device=b.device)
+        tt = torch.tensor([ties, rescans], dtype=torch.int64, device=getattr(b, "device", "cpu"))
         comm.allreduce_sum_(tt)
         ties, rescans = (int(x) for x in tt.tolist())
     if ties:
@@ -370,8 +405,7 @@ def run_pipeline(
     """
     if engine not in ENGINES:
         raise ValueError(f"engine must be one of {ENGINES}, got {engine!r}")
-    x = np.asarray(points, dtype=np.float64)
-    n, d = x.shape if x.ndim == 2 else (0, 0)
+    x = points if _is_device_tensor(points) else np.asarray(points, dtype=np.float64)
     nworkers = resolve_workers(workers) if engine == "par" else 1
     b = backend()
     torch = b.torch
@@ -379,6 +413,7 @@ def run_pipeline(
     t_start = time.perf_counter()
     t0 = time.perf_counter()
     P = _Points(x, b=b)
+    n, d = P.n, P.d
     need_pass = sigma == "auto" or alpha > 0
     nn = None
     p_loc = None

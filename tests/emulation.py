@@ -1,0 +1,230 @@
+"""CPU stand-in for the device backend (TEST INFRASTRUCTURE ONLY).
+
+Implements the per-shard primitives of engine.CudaBackend with the CPU
+oracle so that the product's multi-rank orchestration in
+paper_1702_04739_b200.pipeline (row sharding, fold-stack exchange in rank
+order, the two MIN all-reduces per Boruvka round, hook/contract replicated on
+every rank) can run under torch.distributed with the gloo backend on a
+machine without a GPU.  The fold-stack wire format is the library's
+(ISOC_FOLD_STACK_BYTES: count, overflow, uint64 id[96], double value[96]).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle as orc
+
+CAP = 96
+NO_KEY = 0x7FFFFFFFFFFFFFFF
+
+
+def _split(n):
+    n2 = n // 2
+    return n2 - n2 % 8
+
+
+def find_leaf(total, pos):
+    s, n, hid = 0, total, 1
+    while n > 128:
+        n2 = _split(n)
+        if pos < s + n2:
+            n, hid = n2, hid * 2
+        else:
+            s, n, hid = s + n2, n - n2, hid * 2 + 1
+    return s, n, hid
+
+
+def leaf_sum(a):
+    n = len(a)
+    if n < 8:
+        r = 0.0
+        for x in a:
+            r += x
+        return r
+    r = [float(x) for x in a[:8]]
+    i = 8
+    while i < n - n % 8:
+        for j in range(8):
+            r[j] += a[i + j]
+        i += 8
+    res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+    while i < n:
+        res += a[i]
+        i += 1
+    return res
+
+
+def push(st, v, h):
+    while st and (h & 1) and st[-1][1] == h - 1:
+        v = st[-1][0] + v
+        st.pop()
+        h >>= 1
+    st.append((v, h))
+
+
+def pack_stack(st) -> torch.Tensor:
+    buf = np.zeros(8 + 16 * CAP, dtype=np.uint8)
+    hdr = np.array([len(st), 0], dtype=np.int32)
+    ids = np.zeros(CAP, dtype=np.uint64)
+    vals = np.zeros(CAP, dtype=np.float64)
+    for i, (v, h) in enumerate(st):
+        ids[i], vals[i] = h, v
+    buf[:8] = hdr.view(np.uint8)
+    buf[8:8 + 8 * CAP] = ids.view(np.uint8)
+    buf[8 + 8 * CAP:] = vals.view(np.uint8)
+    return torch.from_numpy(buf)
+
+
+def unpack_stack(t: torch.Tensor):
+    b = t.numpy()
+    cnt = int(b[:8].view(np.int32)[0])
+    ids = b[8:8 + 8 * CAP].view(np.uint64)
+    vals = b[8 + 8 * CAP:].view(np.float64)
+    return [(float(vals[i]), int(ids[i])) for i in range(cnt)]
+
+
+class MstState:
+    def __init__(self, X, n, lo, hi):
+        self.X, self.n, self.lo, self.hi = X, n, lo, hi
+        self.comp = np.arange(n, dtype=np.int64)
+        self.edges = []
+        self.cand = {}
+
+
+class EmuBackend:
+    name = "emulated-cpu"
+    device = "cpu"
+    torch = torch
+
+    def to_device(self, x):
+        return torch.from_numpy(np.ascontiguousarray(x))
+
+    def empty(self, shape, dtype):
+        return torch.empty(shape, dtype=dtype)
+
+    # K1 restated per shard: row stacks, straddle leaves, merge (the CUDA
+    # algorithm of exact_passes.cu, in Python)
+    def sigma_partial(self, X, n, d, lo, hi, alpha):
+        Xn = X.numpy()
+        total = n * n
+        rows = orc.distance_rows(Xn, lo, hi)
+        flat_row = lambda i: rows[i - lo]  # noqa: E731
+        st = []
+        nn_j = np.zeros(hi - lo, np.int32)
+        nn_d = np.zeros(hi - lo)
+        nn_tie = np.zeros(hi - lo, np.int8)
+        for i in range(lo, hi):
+            rs, re = i * n, (i + 1) * n
+            if i > lo:
+                self._straddle(Xn, n, total, i, st)
+            s, l, h = find_leaf(total, rs)
+            if s < rs:
+                if s + l < re:
+                    s, l, h = find_leaf(total, s + l)
+                else:
+                    l = 0
+            while l > 0 and s + l <= re and not (s + l == total and total % 8):
+                push(st, leaf_sum(flat_row(i)[s - rs:s + l - rs]), h)
+                if s + l >= re:
+                    break
+                s, l, h = find_leaf(total, s + l)
+            r = flat_row(i).copy()
+            r[i] = np.inf
+            j = int(np.argmin(r))
+            nn_j[i - lo], nn_d[i - lo] = j, r[j]
+            r2 = r.copy()
+            r2[j] = np.inf
+            nn_tie[i - lo] = int(r2.min() == r[j])
+        self._straddle(Xn, n, total, hi, st)
+        p = np.zeros(hi - lo) if alpha == 0 else orc.row_folds(Xn, 1.0, alpha, lo, hi)[1]
+        return pack_stack(st), (torch.from_numpy(nn_j), torch.from_numpy(nn_d),
+                                torch.from_numpy(nn_tie)), torch.from_numpy(p)
+
+    @staticmethod
+    def _straddle(Xn, n, total, b, st):
+        if b < n:
+            s, l, h = find_leaf(total, b * n)
+            own = s < b * n and s // n == b - 1
+        else:
+            s, l, h = find_leaf(total, total - 1)
+            own = total % 8 != 0 and s >= (n - 1) * n
+        if own:
+            vals = [orc.pair_distance(Xn, f // n, f % n) for f in range(s, s + l)]
+            push(st, leaf_sum(vals), h)
+
+    def sigma_finish(self, stacks):
+        st = []
+        for q in range(stacks.shape[0]):
+            for v, h in unpack_stack(stacks[q]):
+                push(st, v, h)
+        assert len(st) == 1 and st[0][1] == 1, st
+        return 0.0 + st[0][0]
+
+    def omega(self, X, n, d, lo, hi, sigma):
+        return torch.from_numpy(orc.row_folds(X.numpy(), sigma, 0.0, lo, hi)[0])
+
+    # Boruvka primitives on the shard's rows (exact per-row minima)
+    def mst_create(self, X, n, d, lo, hi):
+        return MstState(X.numpy(), n, lo, hi)
+
+    def mst_round_local(self, h, n, nn=None):
+        cmin = np.full(n, NO_KEY, dtype=np.int64)
+        h.cand = {}
+        for i in range(h.lo, h.hi):
+            r = orc.distance_rows(h.X, i, i + 1)[0]
+            r[h.comp == h.comp[i]] = np.inf
+            j = int(np.argmin(r))
+            if not np.isfinite(r[j]):
+                continue
+            h.cand[i] = (r[j], j)
+            key = int(np.float64(r[j]).view(np.int64))
+            c = h.comp[i]
+            cmin[c] = min(cmin[c], key)
+        return torch.from_numpy(cmin)
+
+    def mst_round_edges(self, h, cmin):
+        cm = cmin.numpy()
+        ce = np.full(h.n, NO_KEY, dtype=np.int64)
+        for i, (w, j) in h.cand.items():
+            c = h.comp[i]
+            if int(np.float64(w).view(np.int64)) == cm[c]:
+                ce[c] = min(ce[c], (min(i, j) << 32) | max(i, j))
+        return torch.from_numpy(ce)
+
+    def mst_round_finish(self, h, cmin, cedge):
+        cm, ce = cmin.numpy(), cedge.numpy()
+        comp = h.comp
+        reps = np.flatnonzero(comp == np.arange(h.n))
+        succ = np.arange(h.n)
+        for c in reps:
+            if ce[c] == NO_KEY:
+                continue
+            a, b = int(ce[c]) >> 32, int(ce[c]) & 0xFFFFFFFF
+            succ[c] = comp[b] if comp[a] == c else comp[a]
+        succ2 = succ.copy()
+        for c in reps:
+            s = succ[c]
+            if s != c and succ[s] == c and c < s:
+                s = c
+            succ2[c] = s
+            if s != c:
+                a, b = int(ce[c]) >> 32, int(ce[c]) & 0xFFFFFFFF
+                h.edges.append((a, b, float(np.int64(cm[c]).view(np.float64))))
+        for _ in range(64):
+            nxt = succ2[succ2]
+            if np.array_equal(nxt, succ2):
+                break
+            succ2 = nxt
+        h.comp = succ2[comp]
+        return int(np.sum(h.comp == np.arange(h.n))), 0, 0
+
+    def mst_edges(self, h, n):
+        e = sorted(h.edges)
+        u = torch.tensor([a for a, _, _ in e], dtype=torch.int32)
+        v = torch.tensor([b for _, b, _ in e], dtype=torch.int32)
+        w = torch.tensor([x for _, _, x in e], dtype=torch.float64)
+        return u, v, w
+
+    def mst_destroy(self, h):
+        pass

@@ -1,0 +1,79 @@
+"""Multi-rank host logic on CPU (gloo, world sizes 1/2/3).
+
+Runs the product's sharded orchestration (pipeline._sigma_pass /
+_sigma_from_stack / _boruvka and Comm.allgather_rows) with the CPU
+emulation backend (tests/emulation.py) and checks that sigma, the MST edge
+set and omega are identical for every world size and equal to the oracle
+(reference semantics).  The GPU kernels behind the same primitives are
+checked separately in test_gpu_parity.py.
+"""
+from __future__ import annotations
+
+import os
+import pickle
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n, d, k, out_path):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    for p in (os.path.dirname(here), here, os.path.join(os.path.dirname(here), "oracle")):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle as orc
+    from emulation import EmuBackend
+    from paper_1702_04739_b200 import pipeline as pl
+    from paper_1702_04739_b200.engine import Comm
+
+    X, _ = orc.generate_random(n, d, k, 3)
+    comm = Comm()
+    P = pl._Points(X, comm=comm, b=EmuBackend())
+    stack, nn, _ = pl._sigma_pass(P, 0.0)
+    sigma = pl._sigma_from_stack(P, stack)
+    u, v, w, stats = pl._boruvka(P, nn)
+    omega = comm.allgather_rows(P.b.omega(P.X, n, d, P.lo, P.hi, sigma), n)
+    if rank == 0:
+        edges = sorted((min(a, b), max(a, b), c) for a, b, c in zip(u.tolist(), v.tolist(), w.tolist()))
+        with open(out_path, "wb") as fh:
+            pickle.dump({"sigma": sigma, "edges": edges, "omega": omega.numpy(), "stats": stats}, fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(world, n, d, k):
+    with tempfile.TemporaryDirectory() as tmp:
+        out = os.path.join(tmp, "r.pkl")
+        mp.spawn(_worker, args=(world, _free_port(), n, d, k, out), nprocs=world, join=True)
+        with open(out, "rb") as fh:
+            return pickle.load(fh)
+
+
+@pytest.mark.parametrize("n,d,k", [(150, 3, 4), (203, 2, 3)])
+def test_sharded_host_logic_matches_single_rank_and_oracle(n, d, k, oracle_mod):
+    X, _ = oracle_mod.generate_random(n, d, k, 3)
+    res = {w: _run(w, n, d, k) for w in (1, 2, 3)}
+    ref_sigma = oracle_mod.auto_sigma(X)
+    tree = oracle_mod.prim_mst(X, ref_sigma)
+    prim_edges = sorted((min(u, int(p)), max(u, int(p))) for u, p in enumerate(tree.parent) if p >= 0)
+    omega, _ = oracle_mod.row_folds(X, ref_sigma)
+    for w, r in res.items():
+        assert r["sigma"] == ref_sigma, w
+        assert [(a, b) for a, b, _ in r["edges"]] == prim_edges, w
+        assert np.array_equal(r["omega"].view(np.int64), omega.view(np.int64)), w
+        assert r["edges"] == res[1]["edges"]
