@@ -51,6 +51,7 @@ SIGNATURES = {
     "isoc_sigma_partial": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P, P, P, P, P]),
     "isoc_sigma_finish": (ctypes.c_int, [P, I64, PD, P]),
     "isoc_omega": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P]),
+    "isoc_omega_mst": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P, P, P, P, P]),
     "isoc_mst_create": (ctypes.c_int, [P, I64, I32, I64, I64, P, ctypes.POINTER(P)]),
     "isoc_mst_round_local": (ctypes.c_int, [P, ctypes.c_int, P, P, P, P]),
     "isoc_mst_round_edges": (ctypes.c_int, [P, P, P]),
@@ -65,6 +66,10 @@ SIGNATURES = {
     "isoc_witness": (ctypes.c_int, [P, I32, I64, P, P, P, P, PD]),
     "isoc_tree_destroy": (None, [P]),
     "isoc_exp_dev": (ctypes.c_int, [P, P, I64, P]),
+    "isoc_launch_count": (ctypes.c_longlong, []),
+    "isoc_prof_enable": (None, [ctypes.c_int]),
+    "isoc_prof_read": (ctypes.c_int, [ctypes.c_int, PD, ctypes.POINTER(ctypes.c_longlong)]),
+    "isoc_peak_tflops": (ctypes.c_int, [ctypes.c_int, PD]),
 }
 
 

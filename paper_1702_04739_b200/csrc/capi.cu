@@ -20,6 +20,21 @@ static_assert(sizeof(FoldStack) == ISOC_FOLD_STACK_BYTES, "fold stack layout");
 namespace {
 thread_local std::string g_err;
 
+// Keep freed stream-ordered allocations cached in the device's default pool
+// (the default release threshold of 0 unmaps them at every synchronize, and
+// re-mapping GBs of per-pass scratch costs hundreds of ms per pipeline run).
+void ensure_pool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
 int fail(int code, const char* fmt, ...) {
     char buf[512];
     va_list ap;
@@ -42,12 +57,14 @@ int fail(int code, const char* fmt, ...) {
     } while (0)
 
 template <typename T>
-cudaError_t dalloc(T** p, size_t count) {
-    return cudaMalloc(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T));
+cudaError_t dalloc(T** p, size_t count, cudaStream_t st) {
+    ensure_pool();
+    return cudaMallocAsync(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), st);
 }
 
 template <typename T>
 cudaError_t aalloc(T** p, size_t count, cudaStream_t st) {
+    ensure_pool();
     return cudaMallocAsync(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), st);
 }
 
@@ -178,16 +195,6 @@ int isoc_sigma_finish(const void* stacks_dev, int64_t nseg, double* total_host, 
     return ISOC_OK;
 }
 
-// ------------------------------------------------------------------ omega
-int isoc_omega(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi, double sigma,
-               double* omega, void* stream) {
-    if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
-    if (!(sigma > 0.0)) return fail(ISOC_EINVAL, "sigma must be > 0, got %g", sigma);
-    if (lo < 0 || hi > n || lo >= hi) return fail(ISOC_EINVAL, "bad row range");
-    CK(launch_omega_pass(X, n, d, lo, hi, sigma, omega, (cudaStream_t)stream));
-    return ISOC_OK;
-}
-
 // -------------------------------------------------------------------- MST
 struct isoc_mst {
     const double* X;
@@ -217,7 +224,7 @@ static void mst_free(isoc_mst* h) {
                     h->compB, h->cand_d, h->cand_j, h->cand_state, h->cand_tie, h->rescan_list,
                     h->counters, h->succ, h->succ2, h->eu, h->ev, h->ed};
     for (void* p : ptrs)
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, h->st);
     delete h;
 }
 
@@ -244,27 +251,27 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
                         "%s: %s", #expr, cudaGetErrorString(_e)); \
         }                                                      \
     } while (0)
-    MCK(dalloc(&h->Y, (size_t)n * h->dp));
-    MCK(dalloc(&h->ny, n));
-    MCK(dalloc(&h->rad, n));
-    MCK(dalloc(&h->centre, d));
-    MCK(dalloc(&h->rmax, 1));
-    MCK(dalloc(&h->comp, n));
-    MCK(dalloc(&h->a1, h->rows));
-    MCK(dalloc(&h->a2, h->rows));
-    MCK(dalloc(&h->j1, h->rows));
-    MCK(dalloc(&h->compB, n));
-    MCK(dalloc(&h->cand_d, h->rows));
-    MCK(dalloc(&h->cand_j, h->rows));
-    MCK(dalloc(&h->cand_state, h->rows));
-    MCK(dalloc(&h->cand_tie, h->rows));
-    MCK(dalloc(&h->rescan_list, h->rows));
-    MCK(dalloc(&h->counters, 8));
-    MCK(dalloc(&h->succ, n));
-    MCK(dalloc(&h->succ2, n));
-    MCK(dalloc(&h->eu, n));
-    MCK(dalloc(&h->ev, n));
-    MCK(dalloc(&h->ed, n));
+    MCK(dalloc(&h->Y, (size_t)n * h->dp, h->st));
+    MCK(dalloc(&h->ny, n, h->st));
+    MCK(dalloc(&h->rad, n, h->st));
+    MCK(dalloc(&h->centre, d, h->st));
+    MCK(dalloc(&h->rmax, 1, h->st));
+    MCK(dalloc(&h->comp, n, h->st));
+    MCK(dalloc(&h->a1, h->rows, h->st));
+    MCK(dalloc(&h->a2, h->rows, h->st));
+    MCK(dalloc(&h->j1, h->rows, h->st));
+    MCK(dalloc(&h->compB, n, h->st));
+    MCK(dalloc(&h->cand_d, h->rows, h->st));
+    MCK(dalloc(&h->cand_j, h->rows, h->st));
+    MCK(dalloc(&h->cand_state, h->rows, h->st));
+    MCK(dalloc(&h->cand_tie, h->rows, h->st));
+    MCK(dalloc(&h->rescan_list, h->rows, h->st));
+    MCK(dalloc(&h->counters, 8, h->st));
+    MCK(dalloc(&h->succ, n, h->st));
+    MCK(dalloc(&h->succ2, n, h->st));
+    MCK(dalloc(&h->eu, n, h->st));
+    MCK(dalloc(&h->ev, n, h->st));
+    MCK(dalloc(&h->ed, n, h->st));
     MCK(cudaMemsetAsync(h->counters, 0, 8 * sizeof(int32_t), h->st));
     iota_kernel<<<blocks(n, 256), 256, 0, h->st>>>(h->comp, n);
     MCK(cudaGetLastError());
@@ -334,6 +341,36 @@ void isoc_mst_destroy(isoc_mst* h) {
     mst_free(h);
 }
 
+// ------------------------------------------------------------------ omega
+int isoc_omega(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi, double sigma,
+               double* omega, void* stream) {
+    if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
+    if (!(sigma > 0.0)) return fail(ISOC_EINVAL, "sigma must be > 0, got %g", sigma);
+    if (lo < 0 || hi > n || lo >= hi) return fail(ISOC_EINVAL, "bad row range");
+    ensure_pool();
+    CK(launch_omega_pass(X, n, d, lo, hi, sigma, nullptr, omega, nullptr, nullptr, nullptr,
+                         (cudaStream_t)stream));
+    return ISOC_OK;
+}
+
+int isoc_omega_mst(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi, double sigma,
+                   isoc_mst* h, double* omega, int32_t* nn_j, double* nn_d, int8_t* nn_tie,
+                   void* stream) {
+    if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
+    if (!(sigma > 0.0)) return fail(ISOC_EINVAL, "sigma must be > 0, got %g", sigma);
+    if (lo < 0 || hi > n || lo >= hi) return fail(ISOC_EINVAL, "bad row range");
+    ensure_pool();
+    const int32_t* comp = h ? h->comp : nullptr;
+    if (h && (h->lo != lo || h->hi != hi)) return fail(ISOC_EINVAL, "MST handle rows differ");
+    if (lo == 0 && hi == n) {
+        CK(launch_omega_sym(X, n, d, sigma, comp, omega, nn_j, nn_d, nn_tie, (cudaStream_t)stream));
+    } else {
+        CK(launch_omega_pass(X, n, d, lo, hi, sigma, comp, omega, nn_j, nn_d, nn_tie,
+                             (cudaStream_t)stream));
+    }
+    return ISOC_OK;
+}
+
 // ------------------------------------------------------------------- tree
 struct isoc_tree {
     int64_t n, root, levels, max_width;
@@ -358,24 +395,24 @@ static void tree_free(isoc_tree* t) {
                     t->p_v, t->f_pos, t->om_pos, t->p_pos, t->om_w, t->p_w, t->code[0], t->code[1],
                     t->spars[0], t->spars[1], t->excl, t->scratch, t->j_out};
     for (void* p : ptrs)
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, t->st);
     delete t;
 }
 
 static int tree_alloc(isoc_tree* t, int64_t n) {
-    CK(dalloc(&t->bfs, n));
-    CK(dalloc(&t->pos_of, n));
-    CK(dalloc(&t->parent_v, n));
-    CK(dalloc(&t->depth_v, n));
-    CK(dalloc(&t->child_id_v, n));
-    CK(dalloc(&t->pos_parent, n));
-    CK(dalloc(&t->child_lo, n));
-    CK(dalloc(&t->child_cnt, n));
-    CK(dalloc(&t->parent_d, n));
-    CK(dalloc(&t->flow_v, n));
-    CK(dalloc(&t->level_off, n + 2));
-    CK(dalloc(&t->scratch, n + 4096));
-    CK(dalloc(&t->j_out, 4));
+    CK(dalloc(&t->bfs, n, t->st));
+    CK(dalloc(&t->pos_of, n, t->st));
+    CK(dalloc(&t->parent_v, n, t->st));
+    CK(dalloc(&t->depth_v, n, t->st));
+    CK(dalloc(&t->child_id_v, n, t->st));
+    CK(dalloc(&t->pos_parent, n, t->st));
+    CK(dalloc(&t->child_lo, n, t->st));
+    CK(dalloc(&t->child_cnt, n, t->st));
+    CK(dalloc(&t->parent_d, n, t->st));
+    CK(dalloc(&t->flow_v, n, t->st));
+    CK(dalloc(&t->level_off, n + 2, t->st));
+    CK(dalloc(&t->scratch, n + 4096, t->st));
+    CK(dalloc(&t->j_out, 4, t->st));
     return ISOC_OK;
 }
 
@@ -506,11 +543,11 @@ int isoc_tree_set_weights(isoc_tree* t, const double* omega, const double* p, do
     const int64_t n = t->n;
     cudaStream_t st = t->st;
     if (!t->omega_v) {
-        CK(dalloc(&t->omega_v, n)); CK(dalloc(&t->p_v, n));
-        CK(dalloc(&t->f_pos, n)); CK(dalloc(&t->om_pos, n)); CK(dalloc(&t->p_pos, n));
-        CK(dalloc(&t->om_w, n)); CK(dalloc(&t->p_w, n));
-        CK(dalloc(&t->code[0], n)); CK(dalloc(&t->code[1], n));
-        CK(dalloc(&t->excl, n));
+        CK(dalloc(&t->omega_v, n, t->st)); CK(dalloc(&t->p_v, n, t->st));
+        CK(dalloc(&t->f_pos, n, t->st)); CK(dalloc(&t->om_pos, n, t->st)); CK(dalloc(&t->p_pos, n, t->st));
+        CK(dalloc(&t->om_w, n, t->st)); CK(dalloc(&t->p_w, n, t->st));
+        CK(dalloc(&t->code[0], n, t->st)); CK(dalloc(&t->code[1], n, t->st));
+        CK(dalloc(&t->excl, n, t->st));
     }
     CK(cudaMemcpyAsync(t->omega_v, omega, n * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(t->p_v, p, n * 8, cudaMemcpyDeviceToDevice, st));
@@ -539,9 +576,9 @@ int isoc_decide(isoc_tree* t, double N, int64_t k, int32_t slot, int64_t* j_host
     if (slot < 0 || slot > 1) return fail(ISOC_EINVAL, "slot must be 0 or 1");
     cudaStream_t st = t->st;
     if (t->spars_cap[slot] < k) {
-        if (t->spars[slot]) cudaFree(t->spars[slot]);
+        if (t->spars[slot]) cudaFreeAsync(t->spars[slot], t->st);
         t->spars[slot] = nullptr;
-        CK(dalloc(&t->spars[slot], k));
+        CK(dalloc(&t->spars[slot], k, t->st));
         t->spars_cap[slot] = k;
     }
     CK(launch_decide(t->n, t->levels, t->level_off, t->max_width, t->f_pos, t->om_pos, t->p_pos,

@@ -116,30 +116,27 @@ template <typename Epi>
 __device__ __forceinline__ void exact_tiles(const double* __restrict__ XT, int64_t np, int dpad,
                                             int64_t r0, int64_t ntiles, Stage* st, Epi epi) {
     const int nk = dpad / XK;
-    const int64_t total = ntiles * nk;
     double acc[4][4];
+    int buf = 0;
     load_stage(st[0], XT, np, r0, 0, 0);
     cp_commit();
-    for (int64_t it = 0; it < total; ++it) {
-        const int64_t t = it / nk;
-        const int kc = (int)(it % nk);
-        if (kc == 0) {
+    for (int64_t t = 0; t < ntiles; ++t) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int kc = 0; kc < nk; ++kc) {
+            // prefetch the next (tile, chunk) while this one is consumed
+            if (kc + 1 < nk) load_stage(st[buf ^ 1], XT, np, r0, t * XN, kc + 1);
+            else if (t + 1 < ntiles) load_stage(st[buf ^ 1], XT, np, r0, (t + 1) * XN, 0);
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();
+            compute_stage(st[buf], acc);
+            __syncthreads();
+            buf ^= 1;
         }
-        if (it + 1 < total) {
-            const int64_t t1 = (it + 1) / nk;
-            const int kc1 = (int)((it + 1) % nk);
-            load_stage(st[(it + 1) & 1], XT, np, r0, t1 * XN, kc1);
-        }
-        cp_commit();
-        cp_wait<1>();
-        __syncthreads();
-        compute_stage(st[it & 1], acc);
-        __syncthreads();
-        if (kc == nk - 1) epi(t, acc);
+        epi(t, acc);
     }
 }
 
@@ -199,19 +196,16 @@ __device__ __forceinline__ NNState nn_combine(NNState a, NNState b) {
 
 // per-thread running (m1, j1, m2) with columns visited in increasing order
 __device__ __forceinline__ void nn_update(NNState& s, double v, int64_t j) {
-    if (v < s.m1) {
-        s.m2 = s.m1;
-        s.m1 = v;
-        s.j1 = j;
-    } else {
-        s.m2 = fmin(s.m2, v);
-    }
+    const bool lt = v < s.m1;
+    s.m2 = fmin(s.m2, lt ? s.m1 : v);
+    s.m1 = lt ? v : s.m1;
+    s.j1 = lt ? j : s.j1;
 }
 
 // --------------------------------------------------------------- K1
 struct SigmaSmem {
     Stage st[2];
-    double D[XM][XN];
+    double D[XM][XN + 1];
     double st_val[XM][ROW_CAP];
     uint64_t st_id[XM][ROW_CAP];
     double carry[XM][8];
@@ -290,22 +284,23 @@ sigma_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
                 if (lane == 0) counter_push(sm.pc[r], t, s);
             }
         }
-        // octets of row `orow` that complete inside this tile
-        const int64_t tf0 = rs + c0;                              // first flat index of the tile
-        const int64_t tf1 = rs + ((c0 + XN < n) ? c0 + XN : n);   // one past the last
-        // octet o completes here iff 8o+8 in (tf0, tf1]
-        const int64_t o_first = ((tf0 >> 3) > (s_first >> 3)) ? (tf0 >> 3) : (s_first >> 3);
-        const int64_t o_end_excl = ((tf1 < e_last ? tf1 : e_last) >> 3);
-        for (int q = 0; q < XN / 8 + 2; ++q) {
-            const int64_t o = o_first + q;
-            const bool active = (grow < row_hi) && o < o_end_excl && (8 * o + 8 > tf0);
-            if (!__any_sync(0xffffffffu, active)) break;
-            if (active) {
-                const int64_t f = 8 * o + j8;
-                const double v = (f < tf0) ? sm.carry[orow][j8] : sm.D[orow][f - rs - c0];
-                acc8 = __dadd_rn(acc8, v);
-            }
-            const bool ending = active && (8 * o + 8 == leaf_end);
+        // octets of row `orow` that complete inside this tile; offsets are
+        // relative to the tile's first flat index tf0 (32-bit)
+        const int64_t tf0 = rs + c0;
+        const int tlen = (int)((c0 + XN < n) ? XN : (n - c0));
+        const int64_t oabs0 = ((tf0 >> 3) > (s_first >> 3)) ? (tf0 >> 3) : (s_first >> 3);
+        const int64_t lim = (tf0 + tlen < e_last) ? tf0 + tlen : e_last;
+        const int nq = (grow < row_hi) ? (int)((lim >> 3) - oabs0) : 0;
+        const int base = (int)(oabs0 * 8 - tf0);
+        int lend = (int)((leaf_end - tf0 < ((int64_t)1 << 30)) ? leaf_end - tf0 : ((int64_t)1 << 30));
+        int nq_max = nq;
+#pragma unroll
+        for (int off = 8; off < 32; off <<= 1) nq_max = max(nq_max, __shfl_xor_sync(0xffffffffu, nq_max, off));
+        for (int q = 0; q < nq_max; ++q) {
+            const bool active = q < nq;
+            const int f = base + 8 * q + j8;
+            if (active) acc8 = __dadd_rn(acc8, f < 0 ? sm.carry[orow][j8] : sm.D[orow][f]);
+            const bool ending = active && (base + 8 * q + 8 == lend);
             if (__any_sync(0xffffffffu, ending)) {
                 double x = acc8;
                 double y = __shfl_down_sync(0xffffffffu, x, 1);
@@ -328,12 +323,14 @@ sigma_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
                 if (ending) acc8 = 0.0;
                 leaf_end = __shfl_sync(0xffffffffu, leaf_end, lane & ~7);
                 leaf_id = __shfl_sync(0xffffffffu, leaf_id, lane & ~7);
+                lend = (int)((leaf_end - tf0 < ((int64_t)1 << 30)) ? leaf_end - tf0 : ((int64_t)1 << 30));
             }
         }
         // carry the partial octet at the tile end
         {
+            const int64_t tf1 = tf0 + tlen;
             const int64_t f = (tf1 & ~int64_t(7)) + j8;
-            if (grow < row_hi && f < tf1 && f >= tf0) sm.carry[orow][j8] = sm.D[orow][f - rs - c0];
+            if (grow < row_hi && f < tf1 && f >= tf0) sm.carry[orow][j8] = sm.D[orow][f - tf0];
         }
         __syncthreads();
     });
@@ -493,25 +490,41 @@ struct OmegaSmem {
 
 __global__ void __launch_bounds__(XTH, 2)
 omega_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n, int64_t row_lo,
-                  int64_t row_hi, double sigma, double* __restrict__ omega) {
+                  int64_t row_hi, double sigma, const int32_t* __restrict__ comp,
+                  double* __restrict__ omega, int32_t* __restrict__ nn_j, double* __restrict__ nn_d,
+                  int8_t* __restrict__ nn_tie) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     OmegaSmem& sm = *reinterpret_cast<OmegaSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tx = lane, ty = warp;
     const int64_t r0 = row_lo + (int64_t)blockIdx.x * XM;
     const int64_t ntiles = (n + XN - 1) / XN;
+    NNState nn[4];
+    int32_t crow[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        nn[i] = NNState{INFINITY, INFINITY, -1};
+        const int64_t row = r0 + ty + 8 * i;
+        crow[i] = (comp && row < n) ? comp[row] : -1;
+    }
     exact_tiles(XT, np, dpad, r0, ntiles, sm.st, [&](int64_t t, double (&acc)[4][4]) {
         const int64_t c0 = t * XN;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            const int64_t col = c0 + tx + 32 * j;
+            const int32_t cc = (comp && col < n) ? comp[col] : -2;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int i = 0; i < 4; ++i) {
                 const int64_t row = r0 + ty + 8 * i;
-                const int64_t col = c0 + tx + 32 * j;
                 double f = 0.0;
-                if (col < n && col != row) f = isoc_flow(__dsqrt_rn(acc[i][j]), sigma);
+                if (col < n && col != row) {
+                    const double dd = __dsqrt_rn(acc[i][j]);
+                    f = isoc_flow(dd, sigma);
+                    if (comp && cc != crow[i]) nn_update(nn[i], dd, col);
+                }
                 sm.D[ty + 8 * i][tx + 32 * j] = f;
             }
+        }
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -529,10 +542,39 @@ omega_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
             if (row < row_hi) omega[row - row_lo] = counter_flush(sm.pc[r], ntiles);
         }
     }
+    if (comp) {
+        // columns were visited in increasing order per lane: reduce the lanes
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            NNState s = nn[i];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                NNState o;
+                o.m1 = __shfl_xor_sync(0xffffffffu, s.m1, off);
+                o.m2 = __shfl_xor_sync(0xffffffffu, s.m2, off);
+                o.j1 = __shfl_xor_sync(0xffffffffu, s.j1, off);
+                s = nn_combine(s, o);
+            }
+            const int64_t row = r0 + ty + 8 * i;
+            if (lane == 0 && row < row_hi) {
+                nn_j[row - row_lo] = (int32_t)s.j1;
+                nn_d[row - row_lo] = s.m1;
+                nn_tie[row - row_lo] = (int8_t)(s.m2 == s.m1);
+            }
+        }
+    }
 }
 
 // ----------------------------------------------------------- launchers
 size_t sigma_rowstack_entries(int64_t rows) { return (size_t)rows * ROW_CAP; }
+
+cudaError_t launch_transpose_pad(const double* X, int64_t n, int d, int64_t np, int dpad, double* XT,
+                                 cudaStream_t st) {
+    dim3 grid((unsigned)((np + 31) / 32), (unsigned)((dpad + 31) / 32));
+    transpose_pad_kernel<<<grid, dim3(32, 8), 0, st>>>(X, n, d, np, dpad, XT);
+    note_launch();
+    return cudaGetLastError();
+}
 
 static cudaError_t make_xt(const double* X, int64_t n, int d, double** XT, int64_t* np, int* dpad,
                            cudaStream_t st) {
@@ -540,10 +582,7 @@ static cudaError_t make_xt(const double* X, int64_t n, int d, double** XT, int64
     *dpad = (d + XK - 1) / XK * XK;
     cudaError_t e = cudaMallocAsync((void**)XT, (size_t)(*np) * (*dpad) * sizeof(double), st);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)((*np + 31) / 32), (unsigned)((*dpad + 31) / 32));
-    transpose_pad_kernel<<<grid, dim3(32, 8), 0, st>>>(X, n, d, *np, *dpad, *XT);
-    note_launch();
-    return cudaGetLastError();
+    return launch_transpose_pad(X, n, d, *np, *dpad, *XT, st);
 }
 
 cudaError_t launch_sigma_pass(const double* X, int64_t n, int d, int64_t lo, int64_t hi,
@@ -603,7 +642,8 @@ cudaError_t launch_stack_merge(const FoldStack* in, int64_t nin, int G, FoldStac
 }
 
 cudaError_t launch_omega_pass(const double* X, int64_t n, int d, int64_t lo, int64_t hi,
-                              double sigma, double* omega, cudaStream_t st) {
+                              double sigma, const int32_t* comp, double* omega, int32_t* nn_j,
+                              double* nn_d, int8_t* nn_tie, cudaStream_t st) {
     const int64_t rows = hi - lo;
     if (rows <= 0) return cudaSuccess;
     double* XT = nullptr;
@@ -616,7 +656,8 @@ cudaError_t launch_omega_pass(const double* X, int64_t n, int d, int64_t lo, int
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((rows + XM - 1) / XM);
     const int pid = prof_begin(PK_OMEGA, st);
-    omega_pass_kernel<<<grid, XTH, smem, st>>>(XT, np, dpad, n, lo, hi, sigma, omega);
+    omega_pass_kernel<<<grid, XTH, smem, st>>>(XT, np, dpad, n, lo, hi, sigma, comp, omega, nn_j, nn_d,
+                                               nn_tie);
     prof_end(pid, st);
     note_launch();
     cudaFreeAsync(XT, st);

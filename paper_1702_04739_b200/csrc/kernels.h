@@ -22,7 +22,15 @@ cudaError_t launch_sigma_merge_rows(int64_t n, int64_t lo, int64_t hi, int G, co
 cudaError_t launch_stack_merge(const FoldStack* in, int64_t nin, int G, FoldStack* out,
                                int32_t* flags, cudaStream_t st);
 cudaError_t launch_omega_pass(const double* X, int64_t n, int d, int64_t lo, int64_t hi,
-                              double sigma, double* omega, cudaStream_t st);
+                              double sigma, const int32_t* comp, double* omega, int32_t* nn_j,
+                              double* nn_d, int8_t* nn_tie, cudaStream_t st);
+cudaError_t launch_transpose_pad(const double* X, int64_t n, int d, int64_t np, int dpad, double* XT,
+                                 cudaStream_t st);
+
+// omega_sym.cu
+cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, const int32_t* comp,
+                             double* omega, int32_t* nn_j, double* nn_d, int8_t* nn_tie,
+                             cudaStream_t st);
 
 // boruvka.cu
 cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, double* centre, float* Y,

@@ -131,6 +131,18 @@ class CudaBackend:
         check(self.lib.isoc_omega(_ptr(X), n, d, lo, hi, float(sigma), _ptr(out), self.stream))
         return out
 
+    def omega_mst(self, X, n: int, d: int, lo: int, hi: int, sigma: float, h):
+        """omega rows plus the fused Boruvka round-2 minima (exact)."""
+        torch = self.torch
+        rows = hi - lo
+        out = self.empty((rows,), torch.float64)
+        nn_j = self.empty((rows,), torch.int32)
+        nn_d = self.empty((rows,), torch.float64)
+        nn_tie = self.empty((rows,), torch.int8)
+        check(self.lib.isoc_omega_mst(_ptr(X), n, d, lo, hi, float(sigma), h, _ptr(out), _ptr(nn_j),
+                                      _ptr(nn_d), _ptr(nn_tie), self.stream))
+        return out, (nn_j, nn_d, nn_tie)
+
     # -- Boruvka ------------------------------------------------------
     def mst_create(self, X, n: int, d: int, lo: int, hi: int):
         h = ctypes.c_void_p()

@@ -147,44 +147,69 @@ def _sigma_from_stack(P: _Points, stack) -> float:
     return mean
 
 
-def _boruvka(P: _Points, nn=None) -> tuple:
-    """MST edges on the device; returns (u, v, w, stats).
+def _boruvka(P: _Points, nn=None, sigma: Optional[float] = None) -> tuple:
+    """MST edges on the device; returns (u, v, w, omega_local, stats).
 
-    Per round each rank reduces its row shard to per-component 64-bit keys;
-    two MIN all-reduces (weight bits, then packed endpoints of the rows that
-    attain the minimum) make the lexicographic (d, min, max) winner global,
-    after which hooking/contraction is replicated identically on every rank.
+    Round 1 uses the exact nearest neighbours of the sigma pass (when given);
+    when `sigma` is given the exact omega pass runs right after round 1 and
+    also yields round 2 (each row's exact minimum over other components);
+    the remaining rounds use the FP32 filter + exact re-rank.  Per round each
+    rank reduces its row shard to per-component 64-bit keys; two MIN
+    all-reduces (weight bits, then packed endpoints of the rows that attain
+    the minimum) make the lexicographic (d, min, max) winner global, after
+    which hooking/contraction is replicated identically on every rank.
     """
     b, comm, n = P.b, P.comm, P.n
     h = b.mst_create(P.X, n, P.d, P.lo, P.hi)
+    stats = {"boruvka_rounds": 0, "exact_ties": 0, "exact_rescans": 0, "omega_ms": 0.0}
+    omega_loc = None
+
+    def one_round(cand):
+        cmin = b.mst_round_local(h, n, cand)
+        comm.allreduce_min_(cmin)
+        cedge = b.mst_round_edges(h, cmin)
+        comm.allreduce_min_(cedge)
+        c, t, r = b.mst_round_finish(h, cmin, cedge)
+        stats["boruvka_rounds"] += 1
+        stats["exact_ties"] += t
+        stats["exact_rescans"] += r
+        return c
+
     try:
-        comps, rounds, ties, rescans = n, 0, 0, 0
+        comps = n
+        if nn is not None:
+            comps = _progress(one_round(nn), comps, stats)
+        if sigma is not None:
+            t0 = time.perf_counter()
+            omega_loc, nn2 = b.omega_mst(P.X, n, P.d, P.lo, P.hi, sigma, h)
+            if hasattr(b.torch, "cuda") and b.torch.cuda.is_available():
+                b.torch.cuda.synchronize()
+            stats["omega_ms"] = (time.perf_counter() - t0) * 1e3
+            if comps > 1:
+                comps = _progress(one_round(nn2), comps, stats)
         while comps > 1:
-            cmin = b.mst_round_local(h, n, nn if rounds == 0 else None)
-            comm.allreduce_min_(cmin)
-            cedge = b.mst_round_edges(h, cmin)
-            comm.allreduce_min_(cedge)
-            c, t, r = b.mst_round_finish(h, cmin, cedge)
-            rounds += 1
-            ties += t
-            rescans += r
-            if c >= comps:
-                raise RuntimeError(f"Boruvka round {rounds} made no progress ({c} components)")
-            comps = c
+            comps = _progress(one_round(None), comps, stats)
         u, v, w = b.mst_edges(h, n)
     finally:
         b.mst_destroy(h)
     if comm.world > 1:
         import torch
 
-        tt = torch.tensor([ties, rescans], dtype=torch.int64, device=getattr(b, "device", "cpu"))
+        tt = torch.tensor([stats["exact_ties"], stats["exact_rescans"]], dtype=torch.int64,
+                          device=getattr(b, "device", "cpu"))
         comm.allreduce_sum_(tt)
-        ties, rescans = (int(x) for x in tt.tolist())
-    if ties:
+        stats["exact_ties"], stats["exact_rescans"] = (int(x) for x in tt.tolist())
+    if stats["exact_ties"]:
         warnings.warn(
-            f"{ties} exact distance ties at a component minimum: the MST may differ from the "
-            "reference's Prim tie rule (SURVEY 8c, Appendix A.6)", RuntimeWarning, stacklevel=3)
-    return u, v, w, {"boruvka_rounds": rounds, "exact_ties": ties, "exact_rescans": rescans}
+            f"{stats['exact_ties']} exact distance ties at a component minimum: the MST may differ "
+            "from the reference's Prim tie rule (SURVEY 8c, Appendix A.6)", RuntimeWarning, stacklevel=3)
+    return u, v, w, omega_loc, stats
+
+
+def _progress(c: int, comps: int, stats: dict) -> int:
+    if c >= comps:
+        raise RuntimeError(f"Boruvka round {stats['boruvka_rounds']} made no progress ({c} components)")
+    return c
 
 
 def _rooted_tree_view(dt: DeviceTree, root: int) -> RootedTree:
@@ -222,7 +247,7 @@ def minimum_spanning_tree(points, sigma: float, root: int = 0) -> RootedTree:
     P = _Points(points)
     if not (0 <= root < P.n):
         raise ValueError(f"root must be in [0, {P.n}), got {root}")
-    u, v, w, _ = _boruvka(P)
+    u, v, w, _, _ = _boruvka(P)
     dt = P.b.tree_from_edges(u, v, w, P.n, root, sigma)
     return _rooted_tree_view(dt, root)
 
@@ -429,15 +454,19 @@ def run_pipeline(
     t0 = time.perf_counter()
     if not (0 <= root < n):
         raise ValueError(f"root must be in [0, {n}), got {root}")
-    u, v, w, stats = _boruvka(P, nn)
+    # the exact omega pass runs inside the MST loop (it also yields Boruvka
+    # round 2); its time is booked under "affinity" like the reference's
+    # node_weights
+    u, v, w, om_loc, stats = _boruvka(P, nn, sigma=sigma_val)
     dt = b.tree_from_edges(u, v, w, n, root, sigma_val)
     torch.cuda.synchronize()
-    mst_ms = (time.perf_counter() - t0) * 1e3
+    mst_ms = (time.perf_counter() - t0) * 1e3 - stats["omega_ms"]
+    affinity_ms += stats["omega_ms"]
 
     t0 = time.perf_counter()
     if alpha < 0:
         raise ValueError(f"alpha must be >= 0, got {alpha}")
-    om = P.comm.allgather_rows(b.omega(P.X, n, d, P.lo, P.hi, sigma_val), n)
+    om = P.comm.allgather_rows(om_loc, n)
     if alpha > 0:
         p = P.comm.allgather_rows(p_loc, n)
     else:

@@ -164,6 +164,11 @@ class EmuBackend:
     def omega(self, X, n, d, lo, hi, sigma):
         return torch.from_numpy(orc.row_folds(X.numpy(), sigma, 0.0, lo, hi)[0])
 
+    def omega_mst(self, X, n, d, lo, hi, sigma, h):
+        om = self.omega(X, n, d, lo, hi, sigma)
+        self.mst_round_local(h, n)   # exact per-row minima for round 2
+        return om, "fused"
+
     # Boruvka primitives on the shard's rows (exact per-row minima)
     def mst_create(self, X, n, d, lo, hi):
         return MstState(X.numpy(), n, lo, hi)

@@ -46,8 +46,8 @@ def _worker(rank, world, port, n, d, k, out_path):
     P = pl._Points(X, comm=comm, b=EmuBackend())
     stack, nn, _ = pl._sigma_pass(P, 0.0)
     sigma = pl._sigma_from_stack(P, stack)
-    u, v, w, stats = pl._boruvka(P, nn)
-    omega = comm.allgather_rows(P.b.omega(P.X, n, d, P.lo, P.hi, sigma), n)
+    u, v, w, om_loc, stats = pl._boruvka(P, nn, sigma=sigma)
+    omega = comm.allgather_rows(om_loc, n)
     if rank == 0:
         edges = sorted((min(a, b), max(a, b), c) for a, b, c in zip(u.tolist(), v.tolist(), w.tolist()))
         with open(out_path, "wb") as fh:
