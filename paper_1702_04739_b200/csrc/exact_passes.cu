@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "leaf.h"
 #include "kernels.h"
 #include "prof.h"
 
@@ -233,15 +234,15 @@ sigma_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
     const int orow = warp + 8 * g;
     const int64_t grow = r0 + orow;
     const int64_t rs = grow * n, re = rs + n;
-    int64_t s_first = re, e_last = re, leaf_end = 0;
-    uint64_t leaf_id = 0;
+    int64_t s_first = re, e_last = re;
+    LeafIter lit;
+    lit.start = 0; lit.len = 0; lit.i = 0; lit.sub = 0; lit.T = 0;
     if (grow < row_hi) {
         Leaf L = find_leaf(total, rs);
         if (L.start < rs) L = (L.start + L.len < re) ? find_leaf(total, L.start + L.len) : Leaf{re, 0, 0};
         if (L.len > 0 && L.start + L.len <= re) {
             s_first = L.start;
-            leaf_end = L.start + L.len;
-            leaf_id = L.hid;
+            lit = leaf_iter_from(total, L.start, L.len, L.hid);
             // the octet stream covers leaves inside the row whose length is a
             // multiple of 8: the row's last leaf is excluded when it straddles
             // into the next row or is the global final leaf with a tail
@@ -292,7 +293,8 @@ sigma_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
         const int64_t lim = (tf0 + tlen < e_last) ? tf0 + tlen : e_last;
         const int nq = (grow < row_hi) ? (int)((lim >> 3) - oabs0) : 0;
         const int base = (int)(oabs0 * 8 - tf0);
-        int lend = (int)((leaf_end - tf0 < ((int64_t)1 << 30)) ? leaf_end - tf0 : ((int64_t)1 << 30));
+        int lend = (int)((lit.start + lit.len - tf0 < ((int64_t)1 << 30)) ? lit.start + lit.len - tf0
+                                                                            : ((int64_t)1 << 30));
         int nq_max = nq;
 #pragma unroll
         for (int off = 8; off < 32; off <<= 1) nq_max = max(nq_max, __shfl_xor_sync(0xffffffffu, nq_max, off));
@@ -311,19 +313,17 @@ sigma_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
                 if (ending && j8 == 0) {
                     x = __dadd_rn(x, y);
                     int cnt = sm.st_cnt[orow], ovf = sm.st_ovf[orow];
-                    stack_push(sm.st_val[orow], sm.st_id[orow], cnt, ROW_CAP, ovf, x, leaf_id);
+                    stack_push(sm.st_val[orow], sm.st_id[orow], cnt, ROW_CAP, ovf, x, lit.hid());
                     sm.st_cnt[orow] = cnt;
                     sm.st_ovf[orow] = ovf;
-                    if (leaf_end < e_last) {
-                        Leaf L = find_leaf(total, leaf_end);
-                        leaf_end = L.start + L.len;
-                        leaf_id = L.hid;
-                    }
                 }
-                if (ending) acc8 = 0.0;
-                leaf_end = __shfl_sync(0xffffffffu, leaf_end, lane & ~7);
-                leaf_id = __shfl_sync(0xffffffffu, leaf_id, lane & ~7);
-                lend = (int)((leaf_end - tf0 < ((int64_t)1 << 30)) ? leaf_end - tf0 : ((int64_t)1 << 30));
+                if (ending) {
+                    acc8 = 0.0;
+                    // all 8 lanes of the group advance the iterator in lockstep
+                    if (lit.start + lit.len < e_last) leaf_next(lit, total);
+                    lend = (int)((lit.start + lit.len - tf0 < ((int64_t)1 << 30)) ? lit.start + lit.len - tf0
+                                                                                : ((int64_t)1 << 30));
+                }
             }
         }
         // carry the partial octet at the tile end
