@@ -65,7 +65,8 @@ def workload(args):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed
+    region by ONE background nvidia-smi process (no forks inside the region)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -73,32 +74,36 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
+        self.proc = None
+        self.path = None
 
     def start(self):
-        def run():
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(
-                        ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                         "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-
-        self._t = threading.Thread(target=run, daemon=True)
-        self._t.start()
+        import tempfile
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
 
     def stop(self) -> dict:
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=10)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
         sm, mx, reasons = [], 0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for s in self.samples:
+        try:
+            lines = open(self.path).read().strip().splitlines()
+        except Exception:
+            lines = []
+        for line in lines:
+            s = [x.strip() for x in line.split(",")]
             try:
                 sm.append(float(s[0]))
                 mx = max(mx, float(s[1]))

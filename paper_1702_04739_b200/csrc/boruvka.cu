@@ -34,9 +34,18 @@ __global__ void fill_u64_kernel(unsigned long long* v, int64_t m, unsigned long 
     if (i < m) v[i] = x;
 }
 
+constexpr int FSTAGES = 3;
+constexpr int FKC = 16;   // k per stage
+
+struct FilterStage {
+    float A[FKC][FM];
+    float B[FKC][FN];
+};
+
 struct FilterSmem {
-    float As[2][FK][FM];
-    float Bs[2][FK][FN];
+    FilterStage st[FSTAGES];
+    int32_t ccomp[4][FN];   // tile metadata ring: prefetch runs up to 2 chunks (tiles) ahead
+    float cnorm[4][FN];
     float red_a1[16][FM];
     float red_a2[16][FM];
     int32_t red_j1[16][FM];
@@ -49,38 +58,68 @@ __device__ __forceinline__ void approx_update(float a, int32_t j, float& a1, int
     a1 = fminf(a1, a);
 }
 
-// Y: n x dp fp32 (dp % 8 == 0), ny: |y|^2 fp32, comp: component ids.
+__device__ __forceinline__ void fcp16(void* dst, const void* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+
+// YT: dp x npad fp32 (transposed, zero padded), ny: |y|^2, comp: component ids
+// (both padded to npad with comp = -3 beyond n).
 __global__ void __launch_bounds__(FT, 1)
-boruvka_filter_kernel(const float* __restrict__ Y, const float* __restrict__ ny,
-                      const int32_t* __restrict__ comp, int64_t n, int dp, int64_t row_lo,
-                      int64_t row_hi, float* __restrict__ out_a1, int32_t* __restrict__ out_j1,
-                      float* __restrict__ out_a2) {
+boruvka_filter_kernel(const float* __restrict__ YT, const float* __restrict__ ny,
+                      const int32_t* __restrict__ comp, int64_t n, int64_t npad, int dp,
+                      int64_t row_lo, int64_t row_hi, float* __restrict__ out_a1,
+                      int32_t* __restrict__ out_j1, float* __restrict__ out_a2) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FilterSmem& sm = *reinterpret_cast<FilterSmem*>(smem_raw);
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;
     const int64_t r0 = row_lo + (int64_t)blockIdx.x * FM;
 
-    // thread rows: ty*4+{0..3}, 64+ty*4+{0..3}; cols: tx*4+{0..3}, 64+tx*4+{0..3}
-    int64_t rows[8];
     int32_t rc[8];
     float rn[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        rows[i] = r0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-        const bool ok = rows[i] < row_hi;
-        rc[i] = ok ? comp[rows[i]] : -2;
-        rn[i] = ok ? ny[rows[i]] : 0.f;
+        const int64_t row = r0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        const bool ok = row < row_hi;
+        rc[i] = ok ? comp[row] : -2;
+        rn[i] = ok ? ny[row] : 0.f;
     }
     float a1[8], a2[8];
     int32_t j1[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) { a1[i] = INFINITY; a2[i] = INFINITY; j1[i] = -1; }
 
-    // global->smem mapping: each thread loads one float4 of A and one of B
-    const int lrow = tid >> 1, lk = (tid & 1) * 4;
-    const int nk = dp / FK;
+    const int nk = dp / FKC;
     const int64_t ntiles = (n + FN - 1) / FN;
+    // linear (tile, chunk) stream through a 3-stage cp.async ring; the column
+    // metadata (comp, |y|^2) of a tile rides with its first chunk
+    int64_t lt = 0;
+    int lk = 0, ls = 0;
+    auto issue = [&]() {
+        if (lt < ntiles) {
+            FilterStage& S = sm.st[ls];
+            const int kk = tid >> 4, part = tid & 15;    // 16 k-rows x 32 chunks of 16 B
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                const int p = part + 16 * m;
+                const int64_t krow = (int64_t)(lk * FKC + kk) * npad;
+                fcp16(&S.A[kk][p * 4], YT + krow + r0 + p * 4);
+                fcp16(&S.B[kk][p * 4], YT + krow + lt * FN + p * 4);
+            }
+            if (lk == 0 && tid < 64) {
+                const int half = tid >> 5, q = tid & 31;
+                if (half == 0) fcp16(&sm.ccomp[lt & 3][q * 4], comp + lt * FN + q * 4);
+                else fcp16(&sm.cnorm[lt & 3][q * 4], ny + lt * FN + q * 4);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        ls = (ls + 1 == FSTAGES) ? 0 : ls + 1;
+        if (++lk == nk) { lk = 0; ++lt; }
+    };
+    issue();
+    issue();
+    int cs = 0;
     for (int64_t t = 0; t < ntiles; ++t) {
         const int64_t c0 = t * FN;
         float acc[8][8];
@@ -88,29 +127,17 @@ boruvka_filter_kernel(const float* __restrict__ Y, const float* __restrict__ ny,
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-
-        auto load = [&](int kc, int buf) {
-            const int64_t ar = r0 + lrow, bc = c0 + lrow;
-            float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
-            if (ar < row_hi) va = *reinterpret_cast<const float4*>(Y + ar * dp + kc * FK + lk);
-            if (bc < n) vb = *reinterpret_cast<const float4*>(Y + bc * dp + kc * FK + lk);
-            sm.As[buf][lk + 0][lrow] = va.x; sm.As[buf][lk + 1][lrow] = va.y;
-            sm.As[buf][lk + 2][lrow] = va.z; sm.As[buf][lk + 3][lrow] = va.w;
-            sm.Bs[buf][lk + 0][lrow] = vb.x; sm.Bs[buf][lk + 1][lrow] = vb.y;
-            sm.Bs[buf][lk + 2][lrow] = vb.z; sm.Bs[buf][lk + 3][lrow] = vb.w;
-        };
-        __syncthreads();
-        load(0, 0);
-        __syncthreads();
         for (int kc = 0; kc < nk; ++kc) {
-            const int buf = kc & 1;
-            if (kc + 1 < nk) load(kc + 1, buf ^ 1);
+            issue();
+            asm volatile("cp.async.wait_group 2;\n" ::);
+            __syncthreads();
+            const FilterStage& S = sm.st[cs];
 #pragma unroll
-            for (int kk = 0; kk < FK; ++kk) {
-                const float4 a_lo = *reinterpret_cast<const float4*>(&sm.As[buf][kk][ty * 4]);
-                const float4 a_hi = *reinterpret_cast<const float4*>(&sm.As[buf][kk][64 + ty * 4]);
-                const float4 b_lo = *reinterpret_cast<const float4*>(&sm.Bs[buf][kk][tx * 4]);
-                const float4 b_hi = *reinterpret_cast<const float4*>(&sm.Bs[buf][kk][64 + tx * 4]);
+            for (int kk = 0; kk < FKC; ++kk) {
+                const float4 a_lo = *reinterpret_cast<const float4*>(&S.A[kk][ty * 4]);
+                const float4 a_hi = *reinterpret_cast<const float4*>(&S.A[kk][64 + ty * 4]);
+                const float4 b_lo = *reinterpret_cast<const float4*>(&S.B[kk][tx * 4]);
+                const float4 b_hi = *reinterpret_cast<const float4*>(&S.B[kk][64 + tx * 4]);
                 const float av[8] = {a_lo.x, a_lo.y, a_lo.z, a_lo.w, a_hi.x, a_hi.y, a_hi.z, a_hi.w};
                 const float bv[8] = {b_lo.x, b_lo.y, b_lo.z, b_lo.w, b_hi.x, b_hi.y, b_hi.z, b_hi.w};
 #pragma unroll
@@ -119,19 +146,21 @@ boruvka_filter_kernel(const float* __restrict__ Y, const float* __restrict__ ny,
                     for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
             }
             __syncthreads();
+            cs = (cs + 1 == FSTAGES) ? 0 : cs + 1;
         }
         // epilogue: approximate squared distance, other-component arg-min
+        const int mb = (int)(t & 3);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const int64_t col = c0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-            const bool cok = col < n;
-            const int32_t cc = cok ? comp[col] : -3;
-            const float cn = cok ? ny[col] : 0.f;
+            const int lc = (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+            const int32_t cc = sm.ccomp[mb][lc];
+            const float cn = sm.cnorm[mb][lc];
+            const int32_t col = (int32_t)(c0 + lc);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 float a = fmaf(-2.f, acc[i][j], rn[i] + cn);
-                a = (cc != rc[i] && cok) ? a : INFINITY;
-                approx_update(a, (int32_t)col, a1[i], j1[i], a2[i]);
+                a = (cc != rc[i]) ? a : INFINITY;
+                approx_update(a, col, a1[i], j1[i], a2[i]);
             }
         }
     }
@@ -168,24 +197,25 @@ boruvka_filter_kernel(const float* __restrict__ Y, const float* __restrict__ ny,
     }
 }
 
-// Centre, round to fp32, pad to dp; norms in the same FFMA order as the dot
-// products; R_i = |y_i| rounded up, for the error bound.
+// Centre, round to fp32 and store transposed (YT[k * npad + i], zero padded
+// to dp x npad); norms in the same FFMA order as the dot products; R_i = |y_i|
+// rounded up, for the error bound.
 __global__ void prep_fp32_kernel(const double* __restrict__ X, const double* __restrict__ centre,
-                                 int64_t n, int d, int dp, float* __restrict__ Y,
+                                 int64_t n, int d, int dp, int64_t npad, float* __restrict__ YT,
                                  float* __restrict__ ny, float* __restrict__ rad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= npad) return;
     float s = 0.f;
     double r2 = 0.0;
     for (int k = 0; k < dp; ++k) {
         float y = 0.f;
-        if (k < d) y = (float)(X[i * d + k] - centre[k]);
-        Y[i * dp + k] = y;
+        if (k < d && i < n) y = (float)(X[i * d + k] - centre[k]);
+        YT[(int64_t)k * npad + i] = y;
         s = fmaf(y, y, s);
         r2 += (double)y * (double)y;
     }
-    ny[i] = s;
-    rad[i] = __double2float_ru(sqrt(r2) * (1.0 + 1e-12));
+    ny[i] = i < n ? s : INFINITY;   // padding columns can never be candidates
+    if (i < n) rad[i] = __double2float_ru(sqrt(r2) * (1.0 + 1e-12));
 }
 
 __global__ void column_mean_kernel(const double* __restrict__ X, int64_t n, int d,
@@ -431,10 +461,10 @@ __global__ void relabel_kernel(int32_t* __restrict__ comp, int64_t n, const int3
 // ------------------------------------------------------------ launchers
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, double* centre, float* Y,
-                             float* ny, float* rad, uint32_t* rmax_bits, cudaStream_t st) {
+cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, int64_t npad, double* centre,
+                             float* Y, float* ny, float* rad, uint32_t* rmax_bits, cudaStream_t st) {
     column_mean_kernel<<<d, 256, 0, st>>>(X, n, d, centre);
-    prep_fp32_kernel<<<blocks_for(n, 256), 256, 0, st>>>(X, centre, n, d, dp, Y, ny, rad);
+    prep_fp32_kernel<<<blocks_for(npad, 256), 256, 0, st>>>(X, centre, n, d, dp, npad, Y, ny, rad);
     cudaMemsetAsync(rmax_bits, 0, sizeof(uint32_t), st);
     max_float_kernel<<<296, 256, 0, st>>>(rad, n, rmax_bits);
     note_launch(3);
@@ -442,16 +472,16 @@ cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, double* 
 }
 
 cudaError_t launch_boruvka_filter(const float* Y, const float* ny, const int32_t* comp, int64_t n,
-                                  int dp, int64_t lo, int64_t hi, float* a1, int32_t* j1, float* a2,
-                                  cudaStream_t st) {
+                                  int64_t npad, int dp, int64_t lo, int64_t hi, float* a1, int32_t* j1,
+                                  float* a2, cudaStream_t st) {
     if (hi <= lo) return cudaSuccess;
     const size_t smem = sizeof(FilterSmem);
     cudaError_t e = cudaFuncSetAttribute(boruvka_filter_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int pid = prof_begin(PK_FILTER, st);
-    boruvka_filter_kernel<<<blocks_for(hi - lo, FM), FT, smem, st>>>(Y, ny, comp, n, dp, lo, hi, a1,
-                                                                       j1, a2);
+    boruvka_filter_kernel<<<blocks_for(hi - lo, FM), FT, smem, st>>>(Y, ny, comp, n, npad, dp, lo, hi,
+                                                                       a1, j1, a2);
     prof_end(pid, st);
     note_launch();
     return cudaGetLastError();

@@ -78,6 +78,12 @@ __global__ void iota_kernel(int32_t* v, int64_t m) {
     if (i < m) v[i] = (int32_t)i;
 }
 
+// component ids 0..n-1; padding columns get -3 (never equal to a row's id)
+__global__ void iota_pad_kernel(int32_t* v, int64_t n, int64_t npad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < npad) v[i] = i < n ? (int32_t)i : -3;
+}
+
 __global__ void exp_kernel(const double* x, double* y, int64_t m) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) y[i] = isoc_exp(x[i]);
@@ -198,7 +204,7 @@ int isoc_sigma_finish(const void* stacks_dev, int64_t nseg, double* total_host, 
 // -------------------------------------------------------------------- MST
 struct isoc_mst {
     const double* X;
-    int64_t n, lo, hi, rows;
+    int64_t n, lo, hi, rows, npad;
     int32_t d, dp;
     cudaStream_t st;
     float cd;
@@ -237,10 +243,11 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
     isoc_mst* h = new isoc_mst();
     memset(h, 0, sizeof(*h));
     h->X = X; h->n = n; h->d = d; h->lo = lo; h->hi = hi; h->rows = hi - lo;
-    h->dp = (d + 7) / 8 * 8;
+    h->dp = (d + 15) / 16 * 16;
+    h->npad = (n + 127) / 128 * 128 + 128;
     h->st = (cudaStream_t)stream;
     // rigorous FP32 Gram error coefficient, inflated ("filter bound")
-    h->cd = (float)((((double)d + 9.0) * 0x1p-24 + 0x1p-30) * 1.0625);
+    h->cd = (float)((((double)h->dp + 9.0) * 0x1p-24 + 0x1p-30) * 1.0625);
 #define MCK(expr)                                              \
     do {                                                       \
         cudaError_t _e = (expr);                               \
@@ -251,12 +258,12 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
                         "%s: %s", #expr, cudaGetErrorString(_e)); \
         }                                                      \
     } while (0)
-    MCK(dalloc(&h->Y, (size_t)n * h->dp, h->st));
-    MCK(dalloc(&h->ny, n, h->st));
+    MCK(dalloc(&h->Y, (size_t)h->npad * h->dp, h->st));
+    MCK(dalloc(&h->ny, h->npad, h->st));
     MCK(dalloc(&h->rad, n, h->st));
     MCK(dalloc(&h->centre, d, h->st));
     MCK(dalloc(&h->rmax, 1, h->st));
-    MCK(dalloc(&h->comp, n, h->st));
+    MCK(dalloc(&h->comp, h->npad, h->st));
     MCK(dalloc(&h->a1, h->rows, h->st));
     MCK(dalloc(&h->a2, h->rows, h->st));
     MCK(dalloc(&h->j1, h->rows, h->st));
@@ -273,9 +280,9 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
     MCK(dalloc(&h->ev, n, h->st));
     MCK(dalloc(&h->ed, n, h->st));
     MCK(cudaMemsetAsync(h->counters, 0, 8 * sizeof(int32_t), h->st));
-    iota_kernel<<<blocks(n, 256), 256, 0, h->st>>>(h->comp, n);
+    iota_pad_kernel<<<blocks(h->npad, 256), 256, 0, h->st>>>(h->comp, n, h->npad);
     MCK(cudaGetLastError());
-    MCK(launch_prep_fp32(X, n, d, h->dp, h->centre, h->Y, h->ny, h->rad, h->rmax, h->st));
+    MCK(launch_prep_fp32(X, n, d, h->dp, h->npad, h->centre, h->Y, h->ny, h->rad, h->rmax, h->st));
 #undef MCK
     *out = h;
     return ISOC_OK;
@@ -288,8 +295,8 @@ int isoc_mst_round_local(isoc_mst* h, int use_nn, const int32_t* nn_j, const dou
         CK(launch_nn_candidates(nn_j, nn_d, nn_tie, h->rows, h->cand_d, h->cand_j, h->cand_state,
                                 h->cand_tie, st));
     } else {
-        CK(launch_boruvka_filter(h->Y, h->ny, h->comp, h->n, h->dp, h->lo, h->hi, h->a1, h->j1, h->a2,
-                                 st));
+        CK(launch_boruvka_filter(h->Y, h->ny, h->comp, h->n, h->npad, h->dp, h->lo, h->hi, h->a1, h->j1,
+                                 h->a2, st));
         CK(launch_boruvka_select(h->X, h->n, h->d, h->a1, h->j1, h->a2, h->rad, h->rmax, h->cd, h->comp,
                                  h->lo, h->hi, h->compB, h->cand_d, h->cand_j, h->cand_state,
                                  h->cand_tie, h->rescan_list, h->counters + 0, st));

@@ -33,11 +33,11 @@ cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, co
                              cudaStream_t st);
 
 // boruvka.cu
-cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, double* centre, float* Y,
-                             float* ny, float* rad, uint32_t* rmax_bits, cudaStream_t st);
+cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, int64_t npad, double* centre,
+                             float* Y, float* ny, float* rad, uint32_t* rmax_bits, cudaStream_t st);
 cudaError_t launch_boruvka_filter(const float* Y, const float* ny, const int32_t* comp, int64_t n,
-                                  int dp, int64_t lo, int64_t hi, float* a1, int32_t* j1, float* a2,
-                                  cudaStream_t st);
+                                  int64_t npad, int dp, int64_t lo, int64_t hi, float* a1, int32_t* j1,
+                                  float* a2, cudaStream_t st);
 cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float* a1,
                                   const int32_t* j1, const float* a2, const float* rad,
                                   const uint32_t* rmax_bits, float cd, const int32_t* comp,
