@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + ["c5"])
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--d", type=int, default=None)
     ap.add_argument("--k", type=int, default=None)
@@ -181,10 +181,51 @@ def reference_arm(args):
 KIND_NAMES = ["sigma_pass", "omega_pass", "boruvka_filter", "decide", "rescan", "bfs", "cost"]
 
 
+def tree_phase_bench(args):
+    """C5: tree phase only on a 50M-vertex random recursive tree, k = 100
+    (tree_from_parent_list + extrema + par_solve_miso), vertices/s."""
+    import torch
+    import paper_1702_04739_b200 as pkg
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+
+    n = args.n or 50_000_000
+    k = args.k or 100
+    parent, flows, omega, p = orc.random_tree_instance(n, 0)
+    w = pkg.NodeWeights(omega=omega, p=p, sigma=1.0, alpha=0.0)
+
+    def step():
+        tree = pkg.tree_from_parent_list(parent, flows)
+        ext = pkg.extrema(tree, w)
+        return pkg.par_solve_miso(tree, w, ext, k)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = step()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    print(json.dumps({
+        "metric": "tree-phase vertices/sec (C5: random spanning tree, 50M vertices, k=100)",
+        "value": n * args.steps / el, "unit": "vertices/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic random recursive tree (PCG64 seed 0), flows 1-U, omega 2-1.9U, p=0",
+        "config": {"workload": f"c5 tree phase N={n} k={k}", "n": n, "k": k},
+        "iterations": res.iterations, "miso": res.miso,
+        "e2e": {"value": n * args.steps / el, "unit": "vertices/s",
+                "h2d_bytes_per_step": n * 24, "d2h_bytes_per_step": n * 17}}), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.config == "c5":
+        return tree_phase_bench(args)
     import torch
     import torch.distributed as dist
 

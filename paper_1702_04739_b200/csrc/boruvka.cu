@@ -245,20 +245,20 @@ __global__ void max_float_kernel(const float* __restrict__ v, int64_t n, uint32_
 }
 
 // ------------------------------------------------------------ selection
-__device__ __forceinline__ float row_bound(float Ri, float Rmax, float cd) {
+__device__ __forceinline__ float row_bound(float Ri, float Rmax, float cd, float cabs) {
     const float s = __fadd_ru(Ri, Rmax);
-    return __fmul_ru(cd, __fmul_ru(s, s));
+    return __fadd_ru(__fmul_ru(cd, __fmul_ru(s, s)), __fmul_ru(cabs, s));
 }
 
 __global__ void comp_bound_kernel(const float* __restrict__ a1, const float* __restrict__ rad,
                                   const int32_t* __restrict__ comp, int64_t lo, int64_t hi,
-                                  const uint32_t* __restrict__ rmax_bits, float cd,
+                                  const uint32_t* __restrict__ rmax_bits, float cd, float cabs,
                                   uint32_t* __restrict__ compB) {
     const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= hi) return;
     const float v = a1[i - lo];
     if (!(v < INFINITY)) return;
-    const float E = row_bound(rad[i], __uint_as_float(*rmax_bits), cd);
+    const float E = row_bound(rad[i], __uint_as_float(*rmax_bits), cd, cabs);
     atomicMin(&compB[comp[i]], float_to_ordered(__fadd_ru(v, E)));
 }
 
@@ -268,7 +268,7 @@ __global__ void candidate_kernel(const double* __restrict__ X, int d, const floa
                                  const int32_t* __restrict__ j1, const float* __restrict__ a2,
                                  const float* __restrict__ rad, const int32_t* __restrict__ comp,
                                  int64_t lo, int64_t hi, const uint32_t* __restrict__ rmax_bits,
-                                 float cd, const uint32_t* __restrict__ compB,
+                                 float cd, float cabs, const uint32_t* __restrict__ compB,
                                  double* __restrict__ cand_d, int32_t* __restrict__ cand_j,
                                  int8_t* __restrict__ cand_state, int32_t* __restrict__ rescan_list,
                                  int32_t* __restrict__ rescan_count) {
@@ -278,7 +278,7 @@ __global__ void candidate_kernel(const double* __restrict__ X, int d, const floa
     cand_state[li] = 0;
     const float v = a1[li];
     if (!(v < INFINITY)) return;
-    const float E = row_bound(rad[i], __uint_as_float(*rmax_bits), cd);
+    const float E = row_bound(rad[i], __uint_as_float(*rmax_bits), cd, cabs);
     const float B = ordered_to_float(compB[comp[i]]);
     if (__fsub_rd(v, E) > B) return;
     if (__fsub_rd(a2[li], E) > __fadd_ru(v, E)) {
@@ -458,6 +458,22 @@ __global__ void relabel_kernel(int32_t* __restrict__ comp, int64_t n, const int3
     if (i == r) atomicAdd(nroots, 1);
 }
 
+__global__ void absmax_kernel(const float* __restrict__ v, int64_t m, uint32_t* __restrict__ out) {
+    float x = 0.f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x = fmaxf(x, fabsf(v[i]));
+    for (int off = 16; off > 0; off >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(x));
+}
+
+cudaError_t launch_absmax(const float* v, int64_t m, uint32_t* out, cudaStream_t st) {
+    cudaMemsetAsync(out, 0, sizeof(uint32_t), st);
+    absmax_kernel<<<296, 256, 0, st>>>(v, m, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ launchers
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
@@ -489,7 +505,7 @@ cudaError_t launch_boruvka_filter(const float* Y, const float* ny, const int32_t
 
 cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float* a1,
                                   const int32_t* j1, const float* a2, const float* rad,
-                                  const uint32_t* rmax_bits, float cd, const int32_t* comp,
+                                  const uint32_t* rmax_bits, float cd, float cabs, const int32_t* comp,
                                   int64_t lo, int64_t hi, uint32_t* compB, double* cand_d,
                                   int32_t* cand_j, int8_t* cand_state, int8_t* cand_tie,
                                   int32_t* rescan_list, int32_t* rescan_count, cudaStream_t st) {
@@ -499,9 +515,9 @@ cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float
     cudaMemsetAsync(rescan_count, 0, sizeof(int32_t), st);
     cudaMemsetAsync(cand_tie, 0, (size_t)rows, st);
     comp_bound_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(a1, rad, comp, lo, hi, rmax_bits, cd,
-                                                              compB);
+                                                              cabs, compB);
     candidate_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(X, d, a1, j1, a2, rad, comp, lo, hi,
-                                                             rmax_bits, cd, compB, cand_d, cand_j,
+                                                             rmax_bits, cd, cabs, compB, cand_d, cand_j,
                                                              cand_state, rescan_list, rescan_count);
     const int pid = prof_begin(PK_RESCAN, st);
     rescan_kernel<<<592, 256, 0, st>>>(X, n, d, comp, lo, rescan_list, rescan_count, cand_d, cand_j,

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -207,7 +208,10 @@ struct isoc_mst {
     int64_t n, lo, hi, rows, npad;
     int32_t d, dp;
     cudaStream_t st;
-    float cd;
+    float cd, cabs;
+    int use_tc;
+    float kscale;
+    uint8_t* img;
     float *Y, *ny, *rad;
     double* centre;
     uint32_t* rmax;
@@ -226,7 +230,7 @@ struct isoc_mst {
 
 static void mst_free(isoc_mst* h) {
     if (!h) return;
-    void* ptrs[] = {h->Y, h->ny, h->rad, h->centre, h->rmax, h->comp, h->a1, h->a2, h->j1,
+    void* ptrs[] = {h->img, h->Y, h->ny, h->rad, h->centre, h->rmax, h->comp, h->a1, h->a2, h->j1,
                     h->compB, h->cand_d, h->cand_j, h->cand_state, h->cand_tie, h->rescan_list,
                     h->counters, h->succ, h->succ2, h->eu, h->ev, h->ed};
     for (void* p : ptrs)
@@ -283,6 +287,33 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
     iota_pad_kernel<<<blocks(h->npad, 256), 256, 0, h->st>>>(h->comp, n, h->npad);
     MCK(cudaGetLastError());
     MCK(launch_prep_fp32(X, n, d, h->dp, h->npad, h->centre, h->Y, h->ny, h->rad, h->rmax, h->st));
+    // tensor-core filter (tcgen05, 3-term FP16 split) for d <= 64 unless ISOC_FILTER=ffma
+    const char* fenv = getenv("ISOC_FILTER");
+    h->use_tc = (d <= 64) && !(fenv && strcmp(fenv, "ffma") == 0);
+    if (h->use_tc) {
+        uint32_t* am = nullptr;
+        MCK(dalloc(&am, 1, h->st));
+        MCK(launch_absmax(h->Y, (int64_t)h->npad * h->dp, am, h->st));
+        uint32_t amb = 0;
+        MCK(cudaMemcpyAsync(&amb, am, 4, cudaMemcpyDeviceToHost, h->st));
+        MCK(cudaStreamSynchronize(h->st));
+        cudaFreeAsync(am, h->st);
+        float amax = 0.f;
+        memcpy(&amax, &amb, 4);
+        int s = 0;  // y * 2^s stays below 2^14 in FP16
+        if (amax > 0.f) s = 14 - (int)ceil(log2((double)amax));
+        if (s > 40) s = 40;
+        if (s < -14) s = -14;
+        const float scale = (float)ldexp(1.0, s);
+        h->kscale = (float)-ldexp(1.0, 1 - 2 * s);
+        // split + tensor-core accumulation bound ("filter bound")
+        h->cd = (float)(((13.0 * 64 + 40.0) * 0x1p-24 + 0x1p-30) * 1.25);
+        h->cabs = (float)(ldexp(1.0, -22 - s) * 8.0 * 2.0);
+        MCK(dalloc(&h->img, tc_image_bytes(n), h->st));
+        MCK(launch_tc_image(h->Y, h->npad, d, scale, n, h->img, h->st));
+    } else {
+        h->cabs = 0.f;
+    }
 #undef MCK
     *out = h;
     return ISOC_OK;
@@ -295,9 +326,14 @@ int isoc_mst_round_local(isoc_mst* h, int use_nn, const int32_t* nn_j, const dou
         CK(launch_nn_candidates(nn_j, nn_d, nn_tie, h->rows, h->cand_d, h->cand_j, h->cand_state,
                                 h->cand_tie, st));
     } else {
-        CK(launch_boruvka_filter(h->Y, h->ny, h->comp, h->n, h->npad, h->dp, h->lo, h->hi, h->a1, h->j1,
-                                 h->a2, st));
-        CK(launch_boruvka_select(h->X, h->n, h->d, h->a1, h->j1, h->a2, h->rad, h->rmax, h->cd, h->comp,
+        if (h->use_tc)
+            CK(launch_filter_tc(h->img, h->ny, h->comp, h->n, h->lo, h->hi, h->kscale, h->a1, h->j1, h->a2,
+                                st));
+        else
+            CK(launch_boruvka_filter(h->Y, h->ny, h->comp, h->n, h->npad, h->dp, h->lo, h->hi, h->a1,
+                                     h->j1, h->a2, st));
+        CK(launch_boruvka_select(h->X, h->n, h->d, h->a1, h->j1, h->a2, h->rad, h->rmax, h->cd, h->cabs,
+                                 h->comp,
                                  h->lo, h->hi, h->compB, h->cand_d, h->cand_j, h->cand_state,
                                  h->cand_tie, h->rescan_list, h->counters + 0, st));
     }

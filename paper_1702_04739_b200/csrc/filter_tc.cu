@@ -1,0 +1,311 @@
+// K3tc: Boruvka candidate filter on the 5th-gen tensor cores (sm_100a).
+//
+// Same contract as boruvka_filter_kernel (per row: best approximate squared
+// distance a1 to a column of another component, its column j1, and the
+// second best a2), computed from a 3-term FP16 split of the centred, scaled
+// points: y*2^s = hi + lo (hi = fp16(y 2^s), lo = fp16(y 2^s - hi)), and
+//   <y_i, y_j> 2^2s ~ hi_i.hi_j + hi_i.lo_j + lo_i.hi_j
+// evaluated by tcgen05.mma kind::f16 with FP32 accumulation in TMEM.
+// Operand images are pre-swizzled in HBM in the UMMA K-major SWIZZLE_128B
+// layout (one 16 KB image per 128 points per part), so a plain 1-D bulk copy
+// (cp.async.bulk, TMA engine) lands them ready for the MMA descriptors.
+//
+// CTA = 256 rows (two 128-row blocks, A resident in smem) x all 128-column
+// tiles.  Warp 0: bulk-copy producer; warp 1: TMEM allocation + MMA issue
+// (one elected lane); warps 2-9: epilogue, one thread per row reading its
+// 128 accumulator columns with tcgen05.ld and keeping (a1, j1, a2).
+// Accumulators are double buffered in TMEM (2 x 256 columns) so the MMA of
+// tile t+1 overlaps the epilogue of tile t.  d <= 64 (one 64-wide K atom);
+// larger d uses the FFMA kernel.
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "prof.h"
+
+namespace isoc {
+
+constexpr int TC_BM = 128;          // rows per block = TMEM lanes
+constexpr int TC_BN = 128;          // columns per tile
+constexpr int TC_STAGES = 4;
+constexpr int TC_EPI = 8;           // epilogue warps
+constexpr int TC_THREADS = 64 + 32 * TC_EPI;
+constexpr int TC_PART = 16384;      // bytes of one 128 x 64 fp16 image
+constexpr int TC_META = 8;
+
+struct TcSmem {
+    uint8_t A[2][2][TC_PART];            // [row block][hi/lo]
+    uint8_t B[TC_STAGES][2][TC_PART];    // [stage][hi/lo]
+    int32_t mcomp[2][TC_BN];             // column metadata staged by the epilogue warps
+    float mnorm[2][TC_BN];
+    uint64_t full[TC_STAGES];
+    uint64_t empty[TC_STAGES];
+    uint64_t afull;
+    uint64_t tfull[2];
+    uint64_t tempty[2];
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// K-major SWIZZLE_128B UMMA shared-memory descriptor (version 1, LBO 16 B,
+// SBO = 8 rows x 128 B)
+__device__ __forceinline__ uint64_t umma_desc(const void* p) {
+    const uint64_t addr = smem_u32(p);
+    return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// kind::f16, FP16 x FP16 -> FP32, both K-major, M = 128, N = 128
+constexpr uint32_t TC_IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(TC_IDESC), "r"(accum));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+          "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tc_update(float a, int32_t j, float& a1, int32_t& j1, float& a2) {
+    const bool lt = a < a1;
+    a2 = fminf(a2, fmaxf(a, a1));
+    j1 = lt ? j : j1;
+    a1 = fminf(a1, a);
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
+                 const int32_t* __restrict__ comp, int64_t n, int64_t row_lo, int64_t row_hi,
+                 float kscale, float* __restrict__ out_a1, int32_t* __restrict__ out_j1,
+                 float* __restrict__ out_a2) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    TcSmem& sm = *reinterpret_cast<TcSmem*>(
+        reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023)));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t blk0 = row_lo / TC_BM + 2 * (int64_t)blockIdx.x;   // first 128-row block
+    const int64_t ntiles = (n + TC_BN - 1) / TC_BN;
+    const int64_t nblocks_total = (n + TC_BM - 1) / TC_BM;
+
+    if (tid == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 1);
+        }
+        mbar_init(&sm.afull, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.tfull[s], 1);
+            mbar_init(&sm.tempty[s], TC_EPI);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+            smem_u32(&sm.tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp == 0) {
+        // ------------------------------------------------ producer
+        if (lane == 0) {
+            mbar_expect_tx(&sm.afull, 4 * TC_PART);
+            for (int r = 0; r < 2; ++r) {
+                const int64_t b = (blk0 + r < nblocks_total) ? blk0 + r : nblocks_total - 1;
+                bulk_g2s(sm.A[r][0], img + (b * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.afull);
+                bulk_g2s(sm.A[r][1], img + (b * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.afull);
+            }
+            for (int64_t t = 0; t < ntiles; ++t) {
+                const int s = (int)(t % TC_STAGES);
+                const uint32_t ph = (uint32_t)((t / TC_STAGES) & 1);
+                if (t >= TC_STAGES) mbar_wait(&sm.empty[s], ph ^ 1);
+                mbar_expect_tx(&sm.full[s], 2 * TC_PART);
+                bulk_g2s(sm.B[s][0], img + (t * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+                bulk_g2s(sm.B[s][1], img + (t * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            mbar_wait(&sm.afull, 0);
+            for (int64_t t = 0; t < ntiles; ++t) {
+                const int s = (int)(t % TC_STAGES);
+                const uint32_t ph = (uint32_t)((t / TC_STAGES) & 1);
+                const int as = (int)(t & 1);
+                if (t >= 2) mbar_wait(&sm.tempty[as], (uint32_t)(((t >> 1) - 1) & 1));
+                mbar_wait(&sm.full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint32_t dcol = tmem + (uint32_t)(as * 256 + r * 128);
+#pragma unroll
+                    for (int step = 0; step < 12; ++step) {
+                        const int pass = step >> 2, kk = step & 3;
+                        // pass 0: hi.hi, 1: hi.lo, 2: lo.hi
+                        const uint64_t da = umma_desc(sm.A[r][pass == 2 ? 1 : 0]) + (uint64_t)(kk * 2);
+                        const uint64_t db = umma_desc(sm.B[s][pass == 1 ? 1 : 0]) + (uint64_t)(kk * 2);
+                        umma_f16(dcol, da, db, step > 0 ? 1u : 0u);
+                    }
+                }
+                umma_commit(&sm.empty[s]);
+                umma_commit(&sm.tfull[as]);
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue
+        const int e = warp - 2;             // 0..7
+        const int q = warp & 3;             // TMEM lane quarter of this warp
+        const int r = e >> 2;               // row block
+        const int lrow = q * 32 + lane;     // row inside the block = TMEM lane
+        const int64_t row = (blk0 + r) * TC_BM + lrow;
+        const bool live = row >= row_lo && row < row_hi;
+        const int32_t rc = live ? comp[row] : -2;
+        const float rn = live ? ny[row] : 0.f;
+        float a1 = INFINITY, a2 = INFINITY;
+        int32_t j1 = -1;
+        const int et = tid - 64;            // 0..255
+        for (int64_t t = 0; t < ntiles; ++t) {
+            const int as = (int)(t & 1);
+            // stage the tile's column metadata (epilogue warps only)
+            if (et < TC_BN) sm.mcomp[as][et] = comp[t * TC_BN + et];
+            else sm.mnorm[as][et - TC_BN] = ny[t * TC_BN + et - TC_BN];
+            asm volatile("bar.sync 1, %0;\n" ::"n"(32 * TC_EPI) : "memory");
+            mbar_wait(&sm.tfull[as], (uint32_t)((t >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(as * 256 + r * 128);
+#pragma unroll 1
+            for (int c = 0; c < TC_BN / 32; ++c) {
+                float v[32];
+                tmem_ld32(tbase + (uint32_t)(c * 32), v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int lc = c * 32 + i;
+                    const float cn = sm.mnorm[as][lc];
+                    float a = fmaf(kscale, v[i], rn + cn);
+                    a = (sm.mcomp[as][lc] != rc) ? a : INFINITY;
+                    tc_update(a, (int32_t)(t * TC_BN + lc), a1, j1, a2);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.tempty[as]);
+        }
+        if (live) {
+            out_a1[row - row_lo] = a1;
+            out_j1[row - row_lo] = j1;
+            out_a2[row - row_lo] = a2;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    }
+}
+
+// Pre-swizzled FP16 split images: img[(block * 2 + part) * 16 KB], part 0 = hi,
+// 1 = lo; element (r, k) of a block at (r/8)*1024 + (r%8)*128 + ((k/8)^(r%8))*16 + (k%8)*2.
+__global__ void tc_image_kernel(const float* __restrict__ YT, int64_t npad, int d, float scale,
+                                int64_t nblocks, uint8_t* __restrict__ img) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one (point, k) pair
+    if (idx >= nblocks * TC_BM * 64) return;
+    const int k = (int)(idx & 63);
+    const int64_t p = idx >> 6;
+    const int64_t b = p / TC_BM;
+    const int r = (int)(p % TC_BM);
+    const float y = (k < d && p < npad) ? YT[(int64_t)k * npad + p] * scale : 0.f;
+    const __half hi = __float2half_rn(y);
+    const __half lo = __float2half_rn(y - __half2float(hi));
+    const int64_t off = (int64_t)(r >> 3) * 1024 + (r & 7) * 128 + (((k >> 3) ^ (r & 7)) << 4) + (k & 7) * 2;
+    *reinterpret_cast<__half*>(img + (b * 2 + 0) * (int64_t)TC_PART + off) = hi;
+    *reinterpret_cast<__half*>(img + (b * 2 + 1) * (int64_t)TC_PART + off) = lo;
+}
+
+size_t tc_image_bytes(int64_t n) {
+    const int64_t nblocks = (n + TC_BM - 1) / TC_BM;
+    return (size_t)nblocks * 2 * TC_PART;
+}
+
+cudaError_t launch_tc_image(const float* YT, int64_t npad, int d, float scale, int64_t n, uint8_t* img,
+                            cudaStream_t st) {
+    const int64_t nblocks = (n + TC_BM - 1) / TC_BM;
+    const int64_t total = nblocks * TC_BM * 64;
+    tc_image_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(YT, npad, d, scale, nblocks, img);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_filter_tc(const uint8_t* img, const float* ny, const int32_t* comp, int64_t n,
+                             int64_t lo, int64_t hi, float kscale, float* a1, int32_t* j1, float* a2,
+                             cudaStream_t st) {
+    if (hi <= lo) return cudaSuccess;
+    const size_t smem = sizeof(TcSmem) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t b_lo = lo / TC_BM, b_hi = (hi + TC_BM - 1) / TC_BM;
+    const unsigned grid = (unsigned)((b_hi - b_lo + 1) / 2);
+    const int pid = prof_begin(PK_FILTER, st);
+    filter_tc_kernel<<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, a1, j1, a2);
+    prof_end(pid, st);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace isoc

@@ -40,7 +40,7 @@ cudaError_t launch_boruvka_filter(const float* Y, const float* ny, const int32_t
                                   float* a2, cudaStream_t st);
 cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float* a1,
                                   const int32_t* j1, const float* a2, const float* rad,
-                                  const uint32_t* rmax_bits, float cd, const int32_t* comp,
+                                  const uint32_t* rmax_bits, float cd, float cabs, const int32_t* comp,
                                   int64_t lo, int64_t hi, uint32_t* compB, double* cand_d,
                                   int32_t* cand_j, int8_t* cand_state, int8_t* cand_tie,
                                   int32_t* rescan_list, int32_t* rescan_count, cudaStream_t st);
@@ -62,6 +62,15 @@ cudaError_t launch_hook_contract(int32_t* comp, int64_t n, const unsigned long l
                                  const unsigned long long* compE, int32_t* succ, int32_t* succ2,
                                  int32_t* eu, int32_t* ev, double* ed, int32_t* ecount,
                                  int32_t* changed, int32_t* nroots, cudaStream_t st);
+
+// filter_tc.cu
+size_t tc_image_bytes(int64_t n);
+cudaError_t launch_tc_image(const float* YT, int64_t npad, int d, float scale, int64_t n, uint8_t* img,
+                            cudaStream_t st);
+cudaError_t launch_filter_tc(const uint8_t* img, const float* ny, const int32_t* comp, int64_t n,
+                             int64_t lo, int64_t hi, float kscale, float* a1, int32_t* j1, float* a2,
+                             cudaStream_t st);
+cudaError_t launch_absmax(const float* v, int64_t m, uint32_t* out, cudaStream_t st);
 
 // tree.cu
 cudaError_t launch_build_adjacency(const int32_t* eu, const int32_t* ev, const double* ed,

@@ -46,6 +46,8 @@ struct SymSmem {
     int32_t rminj[TBK];
     double cmin[SB];
     int32_t cminj[SB];
+    int32_t comp_r[TBK];       // component ids of the tile's rows / columns
+    int32_t comp_c[TBK];
 };
 
 __device__ __forceinline__ void sym_cp16(void* dst, const void* src) {
@@ -125,6 +127,11 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 sm.rminj[tid] = INT32_MAX;
             }
         }
+        if (kc == 0 && want_min && tid < 2 * TBK) {
+            const int64_t g = (tid < TBK) ? R0 + ti * TBK + tid : C0 + tj * TBK + (tid - TBK);
+            const int32_t v = g < n ? comp[g] : (tid < TBK ? -1 : -2);
+            if (tid < TBK) sm.comp_r[tid] = v; else sm.comp_c[tid - TBK] = v;
+        }
         if (it + 1 < total) {
             const int t1 = (it + 1) / nk, k1 = (it + 1) % nk;
             sym_load(sm.st[(it + 1) & 1], XT, np, R0 + (t1 >> 3) * TBK, C0 + (t1 & 7) * TBK, k1);
@@ -158,33 +165,63 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
         // ------------------------------------------------ tile epilogue
         const int64_t gr0 = R0 + ti * TBK + rg * 4;   // first global row of this thread
         const int64_t gc0 = C0 + tj * TBK + cg * 8;   // first global col
-        int32_t crow[4], ccol[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = __dsqrt_rn(acc[i][j]);
         if (want_min) {
+            // row minima (columns ascend within the thread; ties -> smaller column)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) crow[i] = (gr0 + i < n) ? comp[gr0 + i] : -1;
+            for (int i = 0; i < 4; ++i) {
+                const int32_t cr = sm.comp_r[rg * 4 + i];
+                double m = INFINITY;
+                int32_t mj = INT32_MAX;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ccol[j] = (gc0 + j < n) ? comp[gc0 + j] : -2;
+                for (int j = 0; j < 8; ++j) {
+                    const int64_t gi = gr0 + i, gj = gc0 + j;
+                    const bool ok = gi < n && gj < n && sm.comp_c[cg * 8 + j] != cr;
+                    if (ok && acc[i][j] < m) { m = acc[i][j]; mj = (int32_t)gj; }
+                }
+#pragma unroll
+                for (int off = 1; off < 8; off <<= 1) {
+                    const double om = __shfl_xor_sync(0xffffffffu, m, off);
+                    const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
+                    if (lex_less(om, oj, m, mj)) { m = om; mj = oj; }
+                }
+                if ((lane & 7) == 0) { sm.xrm[wc][rg * 4 + i] = m; sm.xrj[wc][rg * 4 + i] = mj; }
+            }
+            // column minima (rows ascend within the thread)
+            if (!diag) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int32_t cc = sm.comp_c[cg * 8 + j];
+                    double m = INFINITY;
+                    int32_t mj = INT32_MAX;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int64_t gi = gr0 + i, gj = gc0 + j;
+                        const bool ok = gi < n && gj < n && sm.comp_r[rg * 4 + i] != cc;
+                        if (ok && acc[i][j] < m) { m = acc[i][j]; mj = (int32_t)gi; }
+                    }
+#pragma unroll
+                    for (int off = 8; off < 32; off <<= 1) {
+                        const double om = __shfl_xor_sync(0xffffffffu, m, off);
+                        const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
+                        if (lex_less(om, oj, m, mj)) { m = om; mj = oj; }
+                    }
+                    if ((lane >> 3) == 0) { sm.xcm[wr][cg * 8 + j] = m; sm.xcj[wr][cg * 8 + j] = mj; }
+                }
+            }
         }
-        double rm[4], cm[8];
-        int32_t rj[4], cj[8];
+        // flows in place (diagonal and padding -> 0)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { rm[i] = INFINITY; rj[i] = INT32_MAX; }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) { cm[j] = INFINITY; cj[j] = INT32_MAX; }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int64_t gi = gr0 + i, gj = gc0 + j;
                 const bool valid = gi < n && gj < n && gi != gj;
-                const double dd = __dsqrt_rn(acc[i][j]);
-                if (want_min && valid && crow[i] != ccol[j]) {
-                    if (dd < rm[i]) { rm[i] = dd; rj[i] = (int32_t)gj; }   // columns ascend
-                    if (dd < cm[j]) { cm[j] = dd; cj[j] = (int32_t)gi; }   // rows ascend
-                }
-                acc[i][j] = valid ? isoc_flow(dd, sigma) : 0.0;
+                acc[i][j] = valid ? isoc_flow(acc[i][j], sigma) : 0.0;
             }
-        }
         // row folds: 8 own columns, then 8 lanes, then the two column halves
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -196,17 +233,6 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
             if ((lane & 3) == 0) x = __dadd_rn(x, y);
             y = __shfl_down_sync(0xffffffffu, x, 4);
             if ((lane & 7) == 0) sm.xrow[wc][rg * 4 + i] = __dadd_rn(x, y);
-            if (want_min) {
-                double m = rm[i];
-                int32_t mj = rj[i];
-#pragma unroll
-                for (int off = 1; off < 8; off <<= 1) {
-                    const double om = __shfl_xor_sync(0xffffffffu, m, off);
-                    const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
-                    if (lex_less(om, oj, m, mj)) { m = om; mj = oj; }
-                }
-                if ((lane & 7) == 0) { sm.xrm[wc][rg * 4 + i] = m; sm.xrj[wc][rg * 4 + i] = mj; }
-            }
         }
         // column folds: 4 own rows, then the 4 row groups of the warp
         if (!diag) {
@@ -217,17 +243,6 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 if (((lane >> 3) & 1) == 0) x = __dadd_rn(x, y);
                 y = __shfl_down_sync(0xffffffffu, x, 16);
                 if ((lane >> 3) == 0) sm.xcol[wr][cg * 8 + j] = __dadd_rn(x, y);
-                if (want_min) {
-                    double m = cm[j];
-                    int32_t mj = cj[j];
-#pragma unroll
-                    for (int off = 8; off < 32; off <<= 1) {
-                        const double om = __shfl_xor_sync(0xffffffffu, m, off);
-                        const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
-                        if (lex_less(om, oj, m, mj)) { m = om; mj = oj; }
-                    }
-                    if ((lane >> 3) == 0) { sm.xcm[wr][cg * 8 + j] = m; sm.xcj[wr][cg * 8 + j] = mj; }
-                }
             }
         }
         __syncthreads();
