@@ -326,26 +326,31 @@ def main():
     rounds = run.mst_stats.get("boruvka_rounds", 0)
     # algorithmic flops per launch: exact passes 3*d fp64 flops per
     # ordered pair over all n^2 pairs; the FP32 filter 2*d per pair it scans
+    use_tc = d <= 64 and os.environ.get("ISOC_FILTER", "") != "ffma"
     alg = {
         "sigma_pass": 3.0 * d * n * n,
         "omega_pass": 3.0 * d * n * n,
-        "boruvka_filter": 2.0 * d * n * n,
+        # tcgen05 filter: 3 FP16 MMA passes (hi.hi, hi.lo, lo.hi) over K = 64 per pair
+        "boruvka_filter": (3 * 2.0 * 64 if use_tc else 2.0 * d) * n * n,
     }
     # the exact passes' fp64 ops cannot fuse (scipy's separately rounded
     # mul/add), so their ceiling is the DADD/DMUL issue rate = half the
     # measured DFMA flop rate
     fp64_op_peak = fp64_peak.value / 2.0
+    tensor_peak = float(peaks().get("bf16_tflops") or 1590.0)   # fp16 dense = bf16 dense rate
     peak_for = {"sigma_pass": fp64_op_peak, "omega_pass": fp64_op_peak,
-                "boruvka_filter": fp32_peak.value}
+                "boruvka_filter": tensor_peak if use_tc else fp32_peak.value}
     dom = max(kernels, key=lambda kk: kernels[kk]["ms_total"]) if kernels else None
     roofline = None
     if dom in alg:
         per_launch_ms = kernels[dom]["ms_total"] / max(1.0, kernels[dom]["launches"])
         achieved = alg[dom] / (per_launch_ms * 1e-3) / 1e12
-        roofline = {"kernel": dom, "bound": "fp32" if dom == "boruvka_filter" else "fp64",
+        roofline = {"kernel": dom,
+                    "bound": ("tensor" if use_tc else "fp32") if dom == "boruvka_filter" else "fp64",
                     "achieved": achieved, "peak": peak_for[dom], "unit": "TFLOP/s",
                     "frac": achieved / peak_for[dom], "traffic": None,
-                    "peak_source": ("measured FFMA microkernel (isoc_peak_tflops), this GPU"
+                    "peak_source": (("MEASURED_PEAKS.json bf16_tflops (burst)" if use_tc else
+                                     "measured FFMA microkernel (isoc_peak_tflops), this GPU")
                                     if dom == "boruvka_filter" else
                                     "measured DFMA microkernel / 2 (non-fusable DADD/DMUL issue "
                                     "rate), this GPU")}
@@ -381,7 +386,9 @@ def main():
             "kernels": kernels,
             "roofline": roofline,
             "peaks_measured_tflops": {"fp32_ffma": fp32_peak.value, "fp64_dfma": fp64_peak.value,
+                                      "tensor_bf16_file": tensor_peak,
                                       "hbm_gbs_file": peaks().get("hbm_gbs")},
+            "filter": "tcgen05 3xFP16 split" if use_tc else "FP32 FFMA",
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
