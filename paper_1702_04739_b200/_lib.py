@@ -70,6 +70,8 @@ SIGNATURES = {
     "isoc_prof_enable": (None, [ctypes.c_int]),
     "isoc_prof_read": (ctypes.c_int, [ctypes.c_int, PD, ctypes.POINTER(ctypes.c_longlong)]),
     "isoc_peak_tflops": (ctypes.c_int, [ctypes.c_int, PD]),
+    "isoc_div_check": (ctypes.c_int, [ctypes.c_ulonglong, ctypes.c_ulonglong,
+                                      ctypes.POINTER(ctypes.c_ulonglong), PD]),
 }
 
 

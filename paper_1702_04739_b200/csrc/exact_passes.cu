@@ -486,11 +486,12 @@ struct OmegaSmem {
     Stage st[2];
     double D[XM][XN];
     double pc[XM][PC_LEVELS];
+    uint64_t exp_tab[256];
 };
 
 __global__ void __launch_bounds__(XTH, 2)
 omega_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n, int64_t row_lo,
-                  int64_t row_hi, double sigma, const int32_t* __restrict__ comp,
+                  int64_t row_hi, double sigma, double rs, const int32_t* __restrict__ comp,
                   double* __restrict__ omega, int32_t* __restrict__ nn_j, double* __restrict__ nn_d,
                   int8_t* __restrict__ nn_tie) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -499,6 +500,7 @@ omega_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
     const int tx = lane, ty = warp;
     const int64_t r0 = row_lo + (int64_t)blockIdx.x * XM;
     const int64_t ntiles = (n + XN - 1) / XN;
+    for (int e2 = tid; e2 < 256; e2 += XTH) sm.exp_tab[e2] = ISOC_EXP_TAB[e2];
     NNState nn[4];
     int32_t crow[4];
 #pragma unroll
@@ -519,7 +521,7 @@ omega_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
                 double f = 0.0;
                 if (col < n && col != row) {
                     const double dd = __dsqrt_rn(acc[i][j]);
-                    f = isoc_flow(dd, sigma);
+                    f = isoc_flow_fast(dd, sigma, rs, sm.exp_tab);
                     if (comp && cc != crow[i]) nn_update(nn[i], dd, col);
                 }
                 sm.D[ty + 8 * i][tx + 32 * j] = f;
@@ -656,8 +658,8 @@ cudaError_t launch_omega_pass(const double* X, int64_t n, int d, int64_t lo, int
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((rows + XM - 1) / XM);
     const int pid = prof_begin(PK_OMEGA, st);
-    omega_pass_kernel<<<grid, XTH, smem, st>>>(XT, np, dpad, n, lo, hi, sigma, comp, omega, nn_j, nn_d,
-                                               nn_tie);
+    omega_pass_kernel<<<grid, XTH, smem, st>>>(XT, np, dpad, n, lo, hi, sigma, 1.0 / sigma, comp, omega,
+                                               nn_j, nn_d, nn_tie);
     prof_end(pid, st);
     note_launch();
     cudaFreeAsync(XT, st);

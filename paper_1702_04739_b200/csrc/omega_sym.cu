@@ -48,6 +48,7 @@ struct SymSmem {
     int32_t cminj[SB];
     int32_t comp_r[TBK];       // component ids of the tile's rows / columns
     int32_t comp_c[TBK];
+    uint64_t exp_tab[256];     // exp table in shared memory (lane-divergent lookups)
 };
 
 __device__ __forceinline__ void sym_cp16(void* dst, const void* src) {
@@ -87,13 +88,16 @@ __device__ __forceinline__ double csum_push(double* slots, int idx, double v) {
 
 __global__ void __launch_bounds__(STH, 1)
 omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n, int64_t nbs,
-                 double sigma, const int32_t* __restrict__ comp, double* __restrict__ PS,
+                 double sigma, double rs, const int32_t* __restrict__ comp, double* __restrict__ PS,
                  double* __restrict__ PSm, int32_t* __restrict__ PSj) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SymSmem& sm = *reinterpret_cast<SymSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int wr = w >> 1, wc = w & 1;
-    const int rg = wr * 4 + (lane >> 3), cg = wc * 8 + (lane & 7);
+    const int rg = wr * 4 + (lane >> 3), cl = lane & 7;
+    // thread columns (within the tile): wc*64 + 2*cl + 16*q + h, q < 4, h < 2
+    // -> the 8 lanes of a row group read 8 consecutive 16-byte chunks (no
+    //    bank conflicts); pairs (2p, 2p+1) are this thread's, p = cl + 8q
     // triangular decode of blockIdx -> (I, J), I <= J
     const int64_t b = blockIdx.x;
     int64_t J = (int64_t)((sqrt(8.0 * (double)b + 1.0) - 1.0) / 2.0);
@@ -109,6 +113,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
         sm.cmin[e] = INFINITY;
         sm.cminj[e] = INT32_MAX;
     }
+    for (int e = tid; e < 256; e += STH) sm.exp_tab[e] = ISOC_EXP_TAB[e];
     double acc[4][8];
     // linear pipeline over (ti, tj, kc)
     const int total = 64 * nk;
@@ -149,7 +154,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 double bv[8];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const double2 t = *reinterpret_cast<const double2*>(&s.B[kk][cg * 8 + 2 * q]);
+                    const double2 t = *reinterpret_cast<const double2*>(&s.B[kk][wc * 64 + 2 * cl + 16 * q]);
                     bv[2 * q] = t.x;
                     bv[2 * q + 1] = t.y;
                 }
@@ -164,7 +169,8 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
 
         // ------------------------------------------------ tile epilogue
         const int64_t gr0 = R0 + ti * TBK + rg * 4;   // first global row of this thread
-        const int64_t gc0 = C0 + tj * TBK + cg * 8;   // first global col
+        const int64_t gcb = C0 + tj * TBK;             // first global col of the tile
+#define LCOL(j) (wc * 64 + 2 * cl + 16 * ((j) >> 1) + ((j) & 1))
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -178,9 +184,9 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 int32_t mj = INT32_MAX;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const int64_t gi = gr0 + i, gj = gc0 + j;
-                    const bool ok = gi < n && gj < n && sm.comp_c[cg * 8 + j] != cr;
-                    if (ok && acc[i][j] < m) { m = acc[i][j]; mj = (int32_t)gj; }
+                    const int64_t gi = gr0 + i, gj = gcb + LCOL(j);
+                    const bool ok = gi < n && gj < n && sm.comp_c[LCOL(j)] != cr;
+                    if (ok && lex_less(acc[i][j], (int32_t)gj, m, mj)) { m = acc[i][j]; mj = (int32_t)gj; }
                 }
 #pragma unroll
                 for (int off = 1; off < 8; off <<= 1) {
@@ -194,12 +200,12 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
             if (!diag) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const int32_t cc = sm.comp_c[cg * 8 + j];
+                    const int32_t cc = sm.comp_c[LCOL(j)];
                     double m = INFINITY;
                     int32_t mj = INT32_MAX;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const int64_t gi = gr0 + i, gj = gc0 + j;
+                        const int64_t gi = gr0 + i, gj = gcb + LCOL(j);
                         const bool ok = gi < n && gj < n && sm.comp_r[rg * 4 + i] != cc;
                         if (ok && acc[i][j] < m) { m = acc[i][j]; mj = (int32_t)gi; }
                     }
@@ -209,7 +215,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                         const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
                         if (lex_less(om, oj, m, mj)) { m = om; mj = oj; }
                     }
-                    if ((lane >> 3) == 0) { sm.xcm[wr][cg * 8 + j] = m; sm.xcj[wr][cg * 8 + j] = mj; }
+                    if ((lane >> 3) == 0) { sm.xcm[wr][LCOL(j)] = m; sm.xcj[wr][LCOL(j)] = mj; }
                 }
             }
         }
@@ -218,21 +224,28 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const int64_t gi = gr0 + i, gj = gc0 + j;
+                const int64_t gi = gr0 + i, gj = gcb + LCOL(j);
                 const bool valid = gi < n && gj < n && gi != gj;
-                acc[i][j] = valid ? isoc_flow(acc[i][j], sigma) : 0.0;
+                acc[i][j] = valid ? isoc_flow_fast(acc[i][j], sigma, rs, sm.exp_tab) : 0.0;
             }
-        // row folds: 8 own columns, then 8 lanes, then the two column halves
+        // row folds (pow2 tree over the tile's 128 columns): own pairs (level
+        // 1), lanes cl^1, cl^2, cl^4 (levels 2-4, one 16-column block per q),
+        // own q pairs (levels 5-6), then the two column halves (level 7)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            double x = __dadd_rn(__dadd_rn(__dadd_rn(acc[i][0], acc[i][1]), __dadd_rn(acc[i][2], acc[i][3])),
-                                 __dadd_rn(__dadd_rn(acc[i][4], acc[i][5]), __dadd_rn(acc[i][6], acc[i][7])));
-            double y = __shfl_down_sync(0xffffffffu, x, 1);
-            if ((lane & 1) == 0) x = __dadd_rn(x, y);
-            y = __shfl_down_sync(0xffffffffu, x, 2);
-            if ((lane & 3) == 0) x = __dadd_rn(x, y);
-            y = __shfl_down_sync(0xffffffffu, x, 4);
-            if ((lane & 7) == 0) sm.xrow[wc][rg * 4 + i] = __dadd_rn(x, y);
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double x = __dadd_rn(acc[i][2 * q], acc[i][2 * q + 1]);
+                double y = __shfl_down_sync(0xffffffffu, x, 1);
+                if ((cl & 1) == 0) x = __dadd_rn(x, y);
+                y = __shfl_down_sync(0xffffffffu, x, 2);
+                if ((cl & 3) == 0) x = __dadd_rn(x, y);
+                y = __shfl_down_sync(0xffffffffu, x, 4);
+                v[q] = __dadd_rn(x, y);
+            }
+            if (cl == 0)
+                sm.xrow[wc][rg * 4 + i] = __dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3]));
         }
         // column folds: 4 own rows, then the 4 row groups of the warp
         if (!diag) {
@@ -242,7 +255,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 double y = __shfl_down_sync(0xffffffffu, x, 8);
                 if (((lane >> 3) & 1) == 0) x = __dadd_rn(x, y);
                 y = __shfl_down_sync(0xffffffffu, x, 16);
-                if ((lane >> 3) == 0) sm.xcol[wr][cg * 8 + j] = __dadd_rn(x, y);
+                if ((lane >> 3) == 0) sm.xcol[wr][LCOL(j)] = __dadd_rn(x, y);
             }
         }
         __syncthreads();
@@ -363,7 +376,8 @@ cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, co
     if (e != cudaSuccess) return e;
     const int64_t ctas = nbs * (nbs + 1) / 2;
     const int pid = prof_begin(PK_OMEGA, st);
-    omega_sym_kernel<<<(unsigned)ctas, STH, smem, st>>>(XT, np, dpad, n, nbs, sigma, comp, PS, PSm, PSj);
+    omega_sym_kernel<<<(unsigned)ctas, STH, smem, st>>>(XT, np, dpad, n, nbs, sigma, 1.0 / sigma, comp, PS,
+                                                        PSm, PSj);
     prof_end(pid, st);
     omega_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(PS, PSm, PSj, n, nbs, omega, nn_j,
                                                                      nn_d, nn_tie);
