@@ -329,7 +329,8 @@ def main():
     use_tc = d <= 64 and os.environ.get("ISOC_FILTER", "") != "ffma"
     alg = {
         "sigma_pass": 3.0 * d * n * n,
-        "omega_pass": 3.0 * d * n * n,
+        # one GPU: the symmetric kernel computes each unordered pair once
+        "omega_pass": 3.0 * d * (n * (n + 1) / 2 if world == 1 else n * n),
         # tcgen05 filter: 3 FP16 MMA passes (hi.hi, hi.lo, lo.hi) over K = 64 per pair
         "boruvka_filter": (3 * 2.0 * 64 if use_tc else 2.0 * d) * n * n,
     }

@@ -294,23 +294,63 @@ __global__ void candidate_kernel(const double* __restrict__ X, int d, const floa
 }
 
 // Exact rescan of one row per CTA: min (d, j) over other-component columns,
-// plus whether the minimum is attained twice.
+// plus whether the minimum is attained twice.  Each thread keeps four
+// independent distance chains in flight (columns j, j+T, j+2T, j+3T).
+__device__ __forceinline__ void rescan_take(double v, int64_t j, double& m1, double& m2, int64_t& bj) {
+    if (v < m1 || (v == m1 && j < bj)) {
+        m2 = m1;
+        m1 = v;
+        bj = j;
+    } else {
+        m2 = fmin(m2, v);
+    }
+}
+
 __global__ void rescan_kernel(const double* __restrict__ X, int64_t n, int d,
                               const int32_t* __restrict__ comp, int64_t lo,
                               const int32_t* __restrict__ rescan_list,
                               const int32_t* __restrict__ rescan_count, double* __restrict__ cand_d,
                               int32_t* __restrict__ cand_j, int8_t* __restrict__ cand_tie) {
     const int32_t cnt = *rescan_count;
+    __shared__ double xi[512];
     for (int32_t q = blockIdx.x; q < cnt; q += gridDim.x) {
         const int64_t i = rescan_list[q];
         const int32_t ci = comp[i];
+        const bool cached = d <= 512;
+        __syncthreads();
+        if (cached)
+            for (int k = threadIdx.x; k < d; k += blockDim.x) xi[k] = X[i * d + k];
+        __syncthreads();
+        const double* xr = cached ? xi : X + i * d;
         double m1 = INFINITY, m2 = INFINITY;
         int64_t bj = -1;
-        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-            if (comp[j] == ci) continue;
-            const double v = exact_dist(X + i * d, X + j * d, d);
-            if (v < m1) { m2 = m1; m1 = v; bj = j; }
-            else m2 = fmin(m2, v);
+        const int64_t T = blockDim.x;
+        // Each thread walks its columns j = tid, tid+T, ... skipping its own
+        // component, and computes four distances at a time.
+        int64_t j = threadIdx.x;
+        while (true) {
+            int64_t jj[4];
+            int got = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                while (j < n && comp[j] == ci) j += T;
+                jj[u] = j < n ? j : -1;
+                got += j < n;
+                if (j < n) j += T;
+            }
+            if (got == 0) break;
+            double s[4] = {0.0, 0.0, 0.0, 0.0};
+            const double* xj[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xj[u] = X + (jj[u] >= 0 ? jj[u] : 0) * d;
+            for (int k = 0; k < d; ++k) {
+                const double a = xr[k];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) s[u] = exact_sq_step(s[u], a, xj[u][k]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (jj[u] >= 0) rescan_take(__dsqrt_rn(s[u]), jj[u], m1, m2, bj);
         }
         __shared__ double s1[256], s2[256];
         __shared__ int64_t sj[256];

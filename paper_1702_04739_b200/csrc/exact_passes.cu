@@ -34,7 +34,7 @@ constexpr int XM = 32;        // rows per CTA
 constexpr int XN = 128;       // columns per tile
 constexpr int XK = 16;        // k chunk
 constexpr int XTH = 256;      // threads
-constexpr int ROW_CAP = 40;   // per-row stack capacity (<= 2 log2(n/64) + 2 used)
+constexpr int ROW_CAP = kRowCap;  // per-row stack capacity (<= 2 log2(n/64) + 2 used)
 constexpr int PC_LEVELS = 32; // binary-counter levels for pow2 row folds
 
 // Transposed, zero-padded copy of the points: XT[k * np + i] = X[i, k] for
@@ -265,15 +265,27 @@ sigma_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
     const int64_t ntiles = (n + XN - 1) / XN;
     exact_tiles(XT, np, dpad, r0, ntiles, sm.st, [&](int64_t t, double (&acc)[4][4]) {
         const int64_t c0 = t * XN;
+        if (c0 + XN <= n && (c0 >= r0 + XM || c0 + XN <= r0)) {
+            // interior tile: no padding columns, no diagonal
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t row = r0 + ty + 8 * i;
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int64_t col = c0 + tx + 32 * j;
-                const double v = __dsqrt_rn(acc[i][j]);
-                sm.D[ty + 8 * i][tx + 32 * j] = col < n ? v : 0.0;
-                if (col < n && col != row) nn_update(nn[i], v, col);
+                for (int j = 0; j < 4; ++j) {
+                    const double v = __dsqrt_rn(acc[i][j]);
+                    sm.D[ty + 8 * i][tx + 32 * j] = v;
+                    nn_update(nn[i], v, c0 + tx + 32 * j);
+                }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int64_t row = r0 + ty + 8 * i;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int64_t col = c0 + tx + 32 * j;
+                    const double v = __dsqrt_rn(acc[i][j]);
+                    sm.D[ty + 8 * i][tx + 32 * j] = col < n ? v : 0.0;
+                    if (col < n && col != row) nn_update(nn[i], v, col);
+                }
             }
         }
         __syncthreads();
@@ -291,20 +303,54 @@ sigma_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
         const int tlen = (int)((c0 + XN < n) ? XN : (n - c0));
         const int64_t oabs0 = ((tf0 >> 3) > (s_first >> 3)) ? (tf0 >> 3) : (s_first >> 3);
         const int64_t lim = (tf0 + tlen < e_last) ? tf0 + tlen : e_last;
-        const int nq = (grow < row_hi) ? (int)((lim >> 3) - oabs0) : 0;
+        const int nq = (grow < row_hi) ? max(0, (int)((lim >> 3) - oabs0)) : 0;
         const int base = (int)(oabs0 * 8 - tf0);
-        int lend = (int)((lit.start + lit.len - tf0 < ((int64_t)1 << 30)) ? lit.start + lit.len - tf0
-                                                                            : ((int64_t)1 << 30));
+        // Leaves hold >= 8 octets, so at most two leaf ends fall among the
+        // <= 16 octets of a tile: ea / eb = octet count at which they close.
+        int ea = 0, eb = 0;
+        LeafIter lit2 = lit;
+        if (nq > 0) {
+            const int64_t rel = lit.start + lit.len - (tf0 + base);
+            if (rel <= 8 * (int64_t)nq) {
+                ea = (int)(rel >> 3);
+                if (lit.start + lit.len < e_last) {
+                    leaf_next(lit2, total);
+                    const int64_t rel2 = lit2.start + lit2.len - (tf0 + base);
+                    if (rel2 <= 8 * (int64_t)nq) eb = (int)(rel2 >> 3);
+                }
+            }
+        }
         int nq_max = nq;
 #pragma unroll
         for (int off = 8; off < 32; off <<= 1) nq_max = max(nq_max, __shfl_xor_sync(0xffffffffu, nq_max, off));
-        for (int q = 0; q < nq_max; ++q) {
-            const bool active = q < nq;
-            const int f = base + 8 * q + j8;
-            if (active) acc8 = __dadd_rn(acc8, f < 0 ? sm.carry[orow][j8] : sm.D[orow][f]);
-            const bool ending = active && (base + 8 * q + 8 == lend);
+        double pa = 0.0, pb = 0.0;
+        if (nq_max > 0) {
+            // rows with no octets here read in-bounds garbage that is discarded
+            const double* drow = &sm.D[orow][0];
+            const int fb = nq > 0 ? base : 0;
+            {
+                const int f = fb + j8;
+                const double x = f < 0 ? sm.carry[orow][j8] : drow[f];
+                if (nq > 0) acc8 = __dadd_rn(acc8, x);
+                if (ea == 1) { pa = acc8; acc8 = 0.0; }
+            }
+#pragma unroll
+            for (int q = 1; q < 16; ++q) {
+                if (q < nq_max) {
+                    const double x = drow[fb + 8 * q + j8];
+                    if (q < nq) acc8 = __dadd_rn(acc8, x);
+                    if (ea == q + 1) { pa = acc8; acc8 = 0.0; }
+                    if (eb == q + 1) { pb = acc8; acc8 = 0.0; }
+                }
+            }
+        }
+        // close the (at most two) finished leaves: group-combine the eight
+        // lane accumulators, push onto the row's stack, advance the iterator
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const bool ending = (e == 0) ? ea > 0 : eb > 0;
             if (__any_sync(0xffffffffu, ending)) {
-                double x = acc8;
+                double x = (e == 0) ? pa : pb;
                 double y = __shfl_down_sync(0xffffffffu, x, 1);
                 if ((j8 & 1) == 0) x = __dadd_rn(x, y);
                 y = __shfl_down_sync(0xffffffffu, x, 2);
@@ -317,12 +363,12 @@ sigma_pass_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n
                     sm.st_cnt[orow] = cnt;
                     sm.st_ovf[orow] = ovf;
                 }
-                if (ending) {
-                    acc8 = 0.0;
-                    // all 8 lanes of the group advance the iterator in lockstep
-                    if (lit.start + lit.len < e_last) leaf_next(lit, total);
-                    lend = (int)((lit.start + lit.len - tf0 < ((int64_t)1 << 30)) ? lit.start + lit.len - tf0
-                                                                                : ((int64_t)1 << 30));
+            }
+            if (ending) {
+                if (e == 0) {
+                    if (lit.start + lit.len < e_last) lit = lit2;
+                } else if (lit.start + lit.len < e_last) {
+                    leaf_next(lit, total);
                 }
             }
         }

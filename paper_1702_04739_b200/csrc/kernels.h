@@ -7,6 +7,8 @@
 namespace isoc {
 struct FoldStack;
 
+constexpr int kRowCap = 40;   // per-row leaf-stack capacity of the sigma passes
+
 // exact_passes.cu
 size_t sigma_rowstack_entries(int64_t rows);
 cudaError_t launch_sigma_pass(const double* X, int64_t n, int d, int64_t lo, int64_t hi, int want_p,
@@ -26,6 +28,12 @@ cudaError_t launch_omega_pass(const double* X, int64_t n, int d, int64_t lo, int
                               double* nn_d, int8_t* nn_tie, cudaStream_t st);
 cudaError_t launch_transpose_pad(const double* X, int64_t n, int d, int64_t np, int dpad, double* XT,
                                  cudaStream_t st);
+
+// sigma_sym.cu
+bool sigma_sym_applicable(int64_t n, int64_t lo, int64_t hi, int want_p);
+cudaError_t launch_sigma_sym(const double* X, int64_t n, int d, double* row_vals, uint64_t* row_ids,
+                             int32_t* row_cnt, int32_t* flags, int32_t* nn_j, double* nn_d,
+                             int8_t* nn_tie, cudaStream_t st);
 
 // omega_sym.cu
 cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, const int32_t* comp,
