@@ -381,6 +381,146 @@ __global__ void rescan_kernel(const double* __restrict__ X, int64_t n, int d,
     }
 }
 
+// Tiled exact rescan: work item (group of RR rescan rows, chunk of RCW
+// columns); each column tile of 128 points is read once for all RR rows.
+// Per (row, chunk) the lexicographic (d, j) minimum over other-component
+// columns and the second-smallest value (tie flag) go to scratch; the reduce
+// kernel folds the chunks in column order.
+constexpr int RR = 32;
+constexpr int RCW = 32768;
+constexpr int RKC = 16;
+
+__global__ void __launch_bounds__(256, 2)
+rescan_tile_kernel(const double* __restrict__ X, int64_t n, int d, const int32_t* __restrict__ comp,
+                   const int32_t* __restrict__ rescan_list, const int32_t* __restrict__ rescan_count,
+                   int64_t nchunks, double* __restrict__ pm1, double* __restrict__ pm2,
+                   int32_t* __restrict__ pj) {
+    __shared__ double As[RKC][RR];
+    __shared__ double Bs[RKC][129];
+    __shared__ int32_t crow[RR];
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const int64_t cnt = *rescan_count;
+    const int64_t ngroups = (cnt + RR - 1) / RR;
+    const int64_t items = ngroups * nchunks;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const int64_t g = item / nchunks, c = item % nchunks;
+        __syncthreads();
+        if (tid < RR) {
+            const int64_t q = g * RR + tid;
+            crow[tid] = q < cnt ? comp[rescan_list[q]] : INT32_MIN;
+        }
+        double m1[4], m2[4];
+        int32_t j1[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { m1[i] = INFINITY; m2[i] = INFINITY; j1[i] = INT32_MAX; }
+        const int64_t cend = ((c + 1) * RCW < n) ? (c + 1) * RCW : n;
+        for (int64_t t0 = c * RCW; t0 < cend; t0 += 128) {
+            double acc[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+            for (int k0 = 0; k0 < d; k0 += RKC) {
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int idx = tid + 256 * e;
+                    const int r = idx / RKC, kk = idx % RKC;
+                    const int64_t q = g * RR + r;
+                    As[kk][r] = (q < cnt && k0 + kk < d) ? X[(int64_t)rescan_list[q] * d + k0 + kk] : 0.0;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int idx = tid + 256 * e;
+                    const int j = idx / RKC, kk = idx % RKC;
+                    const int64_t col = t0 + j;
+                    Bs[kk][j] = (col < n && k0 + kk < d) ? X[col * d + k0 + kk] : 0.0;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int kk = 0; kk < RKC; ++kk) {
+                    double a[4], bb[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 8 * i];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tx + 32 * j];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[i][j] = exact_sq_step(acc[i][j], a[i], bb[j]);
+                }
+            }
+            // zero-padded k beyond d adds exact zeros: (0-0)^2 = 0
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t col = t0 + tx + 32 * j;
+                if (col >= n) continue;
+                const int32_t cc = comp[col];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (cc == crow[ty + 8 * i]) continue;
+                    const double v = __dsqrt_rn(acc[i][j]);
+                    const bool lt = v < m1[i];
+                    const double cand = lt ? m1[i] : v;
+                    m2[i] = cand < m2[i] ? cand : m2[i];
+                    m1[i] = lt ? v : m1[i];
+                    j1[i] = lt ? (int32_t)col : j1[i];
+                }
+            }
+        }
+        // reduce the 32 column lanes of each row
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double om1 = __shfl_xor_sync(0xffffffffu, m1[i], off);
+                const double om2 = __shfl_xor_sync(0xffffffffu, m2[i], off);
+                const int32_t oj = __shfl_xor_sync(0xffffffffu, j1[i], off);
+                const bool other_first = om1 < m1[i] || (om1 == m1[i] && oj < j1[i]);
+                const double s1 = other_first ? m1[i] : om1;
+                const double s2 = other_first ? om2 : m2[i];
+                m2[i] = s1 < s2 ? s1 : s2;
+                m1[i] = other_first ? om1 : m1[i];
+                j1[i] = other_first ? oj : j1[i];
+            }
+            const int64_t q = g * RR + ty + 8 * i;
+            if (tx == 0 && q < cnt) {
+                pm1[q * nchunks + c] = m1[i];
+                pm2[q * nchunks + c] = m2[i];
+                pj[q * nchunks + c] = j1[i];
+            }
+        }
+    }
+}
+
+__global__ void rescan_reduce_kernel(const int32_t* __restrict__ rescan_list,
+                                     const int32_t* __restrict__ rescan_count, int64_t lo,
+                                     int64_t nchunks, const double* __restrict__ pm1,
+                                     const double* __restrict__ pm2, const int32_t* __restrict__ pj,
+                                     double* __restrict__ cand_d, int32_t* __restrict__ cand_j,
+                                     int8_t* __restrict__ cand_tie) {
+    const int64_t cnt = *rescan_count;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        double m1 = INFINITY, m2 = INFINITY;
+        int32_t j1 = INT32_MAX;
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const double om1 = pm1[q * nchunks + c], om2 = pm2[q * nchunks + c];
+            const int32_t oj = pj[q * nchunks + c];
+            const bool other_first = om1 < m1 || (om1 == m1 && oj < j1);
+            const double s1 = other_first ? m1 : om1;
+            const double s2 = other_first ? om2 : m2;
+            m2 = s1 < s2 ? s1 : s2;
+            m1 = other_first ? om1 : m1;
+            j1 = other_first ? oj : j1;
+        }
+        const int64_t i = rescan_list[q];
+        cand_d[i - lo] = m1;
+        cand_j[i - lo] = j1 == INT32_MAX ? -1 : j1;
+        cand_tie[i - lo] = (int8_t)(m2 == m1);
+    }
+}
+
 // Round 1 from the fused exact nearest neighbours: every row is a candidate.
 __global__ void nn_candidates_kernel(const int32_t* __restrict__ nn_j, const double* __restrict__ nn_d,
                                      const int8_t* __restrict__ nn_tie, int64_t rows,
@@ -559,11 +699,25 @@ cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float
     candidate_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(X, d, a1, j1, a2, rad, comp, lo, hi,
                                                              rmax_bits, cd, cabs, compB, cand_d, cand_j,
                                                              cand_state, rescan_list, rescan_count);
+    const int64_t nchunks = (n + RCW - 1) / RCW;
+    double *pm1 = nullptr, *pm2 = nullptr;
+    int32_t* pj = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&pm1, (size_t)rows * nchunks * 8, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMallocAsync((void**)&pm2, (size_t)rows * nchunks * 8, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMallocAsync((void**)&pj, (size_t)rows * nchunks * 4, st);
+    if (e != cudaSuccess) return e;
     const int pid = prof_begin(PK_RESCAN, st);
-    rescan_kernel<<<592, 256, 0, st>>>(X, n, d, comp, lo, rescan_list, rescan_count, cand_d, cand_j,
-                                       cand_tie);
+    rescan_tile_kernel<<<148 * 3, 256, 0, st>>>(X, n, d, comp, rescan_list, rescan_count, nchunks, pm1,
+                                                pm2, pj);
+    rescan_reduce_kernel<<<148, 256, 0, st>>>(rescan_list, rescan_count, lo, nchunks, pm1, pm2, pj,
+                                              cand_d, cand_j, cand_tie);
     prof_end(pid, st);
-    note_launch(3);
+    note_launch(4);
+    cudaFreeAsync(pm1, st);
+    cudaFreeAsync(pm2, st);
+    cudaFreeAsync(pj, st);
     return cudaGetLastError();
 }
 
