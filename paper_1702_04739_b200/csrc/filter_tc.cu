@@ -30,7 +30,7 @@ namespace isoc {
 constexpr int TC_BM = 128;          // rows per block = TMEM lanes
 constexpr int TC_BN = 128;          // columns per tile
 constexpr int TC_STAGES = 4;
-constexpr int TC_EPI = 8;           // epilogue warps
+constexpr int TC_EPI = 16;          // epilogue warps (2 threads per row, 64 columns each)
 constexpr int TC_THREADS = 64 + 32 * TC_EPI;
 constexpr int TC_PART = 16384;      // bytes of one 128 x 64 fp16 image
 constexpr int TC_META = 8;
@@ -40,6 +40,8 @@ struct TcSmem {
     uint8_t B[TC_STAGES][2][TC_PART];    // [stage][hi/lo]
     int32_t mcomp[2][TC_BN];             // column metadata staged by the epilogue warps
     float mnorm[2][TC_BN];
+    float xa1[2 * TC_BM], xa2[2 * TC_BM];  // second-half partials of each row
+    int32_t xj1[2 * TC_BM];
     uint64_t full[TC_STAGES];
     uint64_t empty[TC_STAGES];
     uint64_t afull;
@@ -209,47 +211,80 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
         }
     } else {
         // ------------------------------------------------ epilogue
-        const int e = warp - 2;             // 0..7
-        const int q = warp & 3;             // TMEM lane quarter of this warp
-        const int r = e >> 2;               // row block
-        const int lrow = q * 32 + lane;     // row inside the block = TMEM lane
+        // warp e = warp - 2 (0..15): TMEM lane quarter warp & 3, row block
+        // (e >> 3), column half (e >> 2) & 1; a row's two threads combine at
+        // the end.  The row norm is added after the minimum (rounding is
+        // monotone, so min / second min commute with + rn).
+        const int e = warp - 2;
+        const int q = warp & 3;
+        const int r = e >> 3;
+        const int hcol = (e >> 2) & 1;
+        const int lrow = q * 32 + lane;
         const int64_t row = (blk0 + r) * TC_BM + lrow;
         const bool live = row >= row_lo && row < row_hi;
         const int32_t rc = live ? comp[row] : -2;
-        const float rn = live ? ny[row] : 0.f;
         float a1 = INFINITY, a2 = INFINITY;
         int32_t j1 = -1;
-        const int et = tid - 64;            // 0..255
+        const int et = tid - 64;            // 0..511
         for (int64_t t = 0; t < ntiles; ++t) {
             const int as = (int)(t & 1);
             // stage the tile's column metadata (epilogue warps only)
             if (et < TC_BN) sm.mcomp[as][et] = comp[t * TC_BN + et];
-            else sm.mnorm[as][et - TC_BN] = ny[t * TC_BN + et - TC_BN];
+            else if (et < 2 * TC_BN) sm.mnorm[as][et - TC_BN] = ny[t * TC_BN + et - TC_BN];
             asm volatile("bar.sync 1, %0;\n" ::"n"(32 * TC_EPI) : "memory");
             mbar_wait(&sm.tfull[as], (uint32_t)((t >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;\n");
-            const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(as * 256 + r * 128);
+            const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(as * 256 + r * 128 + hcol * 64);
 #pragma unroll 1
-            for (int c = 0; c < TC_BN / 32; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 float v[32];
                 tmem_ld32(tbase + (uint32_t)(c * 32), v);
+                const int lc0 = hcol * 64 + c * 32;
+                // masked estimates and their chunk minimum; the top-2 update
+                // can only change (a1, j1, a2) if some value is below a2
+                float m = INFINITY;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int lc = c * 32 + i;
-                    const float cn = sm.mnorm[as][lc];
-                    float a = fmaf(kscale, v[i], rn + cn);
-                    a = (sm.mcomp[as][lc] != rc) ? a : INFINITY;
-                    tc_update(a, (int32_t)(t * TC_BN + lc), a1, j1, a2);
+                for (int i4 = 0; i4 < 8; ++i4) {
+                    const float4 cn4 = *reinterpret_cast<const float4*>(&sm.mnorm[as][lc0 + 4 * i4]);
+                    const int4 cc4 = *reinterpret_cast<const int4*>(&sm.mcomp[as][lc0 + 4 * i4]);
+                    const float cn[4] = {cn4.x, cn4.y, cn4.z, cn4.w};
+                    const int32_t cc[4] = {cc4.x, cc4.y, cc4.z, cc4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = 4 * i4 + u;
+                        const float a = fmaf(kscale, v[i], cn[u]);
+                        v[i] = (cc[u] != rc) ? a : INFINITY;
+                        m = fminf(m, v[i]);
+                    }
+                }
+                if (m < a2) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) tc_update(v[i], (int32_t)(t * TC_BN + lc0 + i), a1, j1, a2);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n");
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.tempty[as]);
         }
-        if (live) {
-            out_a1[row - row_lo] = a1;
+        const int slot = r * TC_BM + lrow;
+        if (hcol == 1) {
+            sm.xa1[slot] = a1;
+            sm.xa2[slot] = a2;
+            sm.xj1[slot] = j1;
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * TC_EPI) : "memory");
+        if (hcol == 0 && live) {
+            // columns of the two halves interleave per tile: lexicographic (a, j)
+            const float b1 = sm.xa1[slot], b2 = sm.xa2[slot];
+            const int32_t bj = sm.xj1[slot];
+            const bool other = b1 < a1 || (b1 == a1 && bj >= 0 && (j1 < 0 || bj < j1));
+            const float lose = other ? a1 : b1;
+            a2 = fminf(fminf(a2, b2), lose);
+            if (other) { a1 = b1; j1 = bj; }
+            const float rn = ny[row];
+            out_a1[row - row_lo] = a1 + rn;
             out_j1[row - row_lo] = j1;
-            out_a2[row - row_lo] = a2;
+            out_a2[row - row_lo] = a2 + rn;
         }
     }
     __syncthreads();
