@@ -34,12 +34,13 @@ constexpr int TC_EPI = 16;          // epilogue warps (2 threads per row, 64 col
 constexpr int TC_THREADS = 64 + 32 * TC_EPI;
 constexpr int TC_PART = 16384;      // bytes of one 128 x 64 fp16 image
 constexpr int TC_META = 8;
+constexpr int TC_MS = 4;            // metadata ring slots
 
 struct TcSmem {
     uint8_t A[2][2][TC_PART];            // [row block][hi/lo]
     uint8_t B[TC_STAGES][2][TC_PART];    // [stage][hi/lo]
-    int32_t mcomp[2][TC_BN];             // column metadata staged by the epilogue warps
-    float mnorm[2][TC_BN];
+    int32_t mcomp[TC_MS][TC_BN];         // column metadata ring (bulk-copied by the producer)
+    float mnorm[TC_MS][TC_BN];
     float xa1[2 * TC_BM], xa2[2 * TC_BM];  // second-half partials of each row
     int32_t xj1[2 * TC_BM];
     uint64_t full[TC_STAGES];
@@ -47,6 +48,8 @@ struct TcSmem {
     uint64_t afull;
     uint64_t tfull[2];
     uint64_t tempty[2];
+    uint64_t mfull[TC_MS];
+    uint64_t mempty[TC_MS];
     uint32_t tmem_base;
 };
 
@@ -152,6 +155,10 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
             mbar_init(&sm.tfull[s], 1);
             mbar_init(&sm.tempty[s], TC_EPI);
         }
+        for (int s = 0; s < TC_MS; ++s) {
+            mbar_init(&sm.mfull[s], 1);
+            mbar_init(&sm.mempty[s], TC_EPI);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 1) {
@@ -180,6 +187,13 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                 mbar_expect_tx(&sm.full[s], 2 * TC_PART);
                 bulk_g2s(sm.B[s][0], img + (t * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
                 bulk_g2s(sm.B[s][1], img + (t * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+                // the tile's column components and norms for the epilogue
+                const int ms = (int)(t % TC_MS);
+                const uint32_t mph = (uint32_t)((t / TC_MS) & 1);
+                if (t >= TC_MS) mbar_wait(&sm.mempty[ms], mph ^ 1);
+                mbar_expect_tx(&sm.mfull[ms], 2 * TC_BN * 4);
+                bulk_g2s(sm.mcomp[ms], comp + t * TC_BN, TC_BN * 4, &sm.mfull[ms]);
+                bulk_g2s(sm.mnorm[ms], ny + t * TC_BN, TC_BN * 4, &sm.mfull[ms]);
             }
         }
     } else if (warp == 1) {
@@ -225,13 +239,10 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
         const int32_t rc = live ? comp[row] : -2;
         float a1 = INFINITY, a2 = INFINITY;
         int32_t j1 = -1;
-        const int et = tid - 64;            // 0..511
         for (int64_t t = 0; t < ntiles; ++t) {
             const int as = (int)(t & 1);
-            // stage the tile's column metadata (epilogue warps only)
-            if (et < TC_BN) sm.mcomp[as][et] = comp[t * TC_BN + et];
-            else if (et < 2 * TC_BN) sm.mnorm[as][et - TC_BN] = ny[t * TC_BN + et - TC_BN];
-            asm volatile("bar.sync 1, %0;\n" ::"n"(32 * TC_EPI) : "memory");
+            const int ms = (int)(t % TC_MS);
+            mbar_wait(&sm.mfull[ms], (uint32_t)((t / TC_MS) & 1));
             mbar_wait(&sm.tfull[as], (uint32_t)((t >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;\n");
             const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(as * 256 + r * 128 + hcol * 64);
@@ -245,8 +256,8 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                 float m = INFINITY;
 #pragma unroll
                 for (int i4 = 0; i4 < 8; ++i4) {
-                    const float4 cn4 = *reinterpret_cast<const float4*>(&sm.mnorm[as][lc0 + 4 * i4]);
-                    const int4 cc4 = *reinterpret_cast<const int4*>(&sm.mcomp[as][lc0 + 4 * i4]);
+                    const float4 cn4 = *reinterpret_cast<const float4*>(&sm.mnorm[ms][lc0 + 4 * i4]);
+                    const int4 cc4 = *reinterpret_cast<const int4*>(&sm.mcomp[ms][lc0 + 4 * i4]);
                     const float cn[4] = {cn4.x, cn4.y, cn4.z, cn4.w};
                     const int32_t cc[4] = {cc4.x, cc4.y, cc4.z, cc4.w};
 #pragma unroll
@@ -264,7 +275,10 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.tempty[as]);
+            if (lane == 0) {
+                mbar_arrive(&sm.tempty[as]);
+                mbar_arrive(&sm.mempty[ms]);
+            }
         }
         const int slot = r * TC_BM + lrow;
         if (hcol == 1) {
