@@ -375,6 +375,16 @@ def main():
                     ex = 3.0 * d * executed_pairs[kk] / (pl_ms * 1e-3) / 1e12
                     v["executed"] = {"pairs": executed_pairs[kk], "tflops": ex,
                                      "frac_of_peak": ex / peak_for[kk]}
+        # DRAM bytes per launch of the dominant kernel from the committed ncu
+        # launch list of the same configuration (bench.py cannot run ncu itself)
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_c3.json")))
+            if tr.get("config") == f"c3 N={n} d={d} k={k}" and dom in tr:
+                roofline["traffic"] = tr[dom]
+                roofline["traffic_unit"] = "bytes per launch"
+                roofline["traffic_source"] = tr["source"]
+        except Exception:
+            pass
         if dom in executed_pairs:
             roofline["executed"] = kernels[dom]["executed"]
             roofline["note"] = ("algorithmic count per SURVEY 8(d) is 3*d flops x all N^2 ordered "

@@ -44,6 +44,15 @@ D = ctypes.c_double
 PI64 = ctypes.POINTER(ctypes.c_int64)
 PD = ctypes.POINTER(ctypes.c_double)
 
+class RunOut(ctypes.Structure):
+    """isoc_run_out (include/isoclust_b200.h)."""
+    _fields_ = [("labels", P), ("cut", P), ("eta", P), ("sparsities", P), ("trace_mid", P),
+                ("trace_ok", P), ("trace_cap", ctypes.c_int32), ("trace_len", ctypes.c_int32),
+                ("iterations", I64), ("clusters_found", I64), ("miso", D), ("sigma", D),
+                ("alpha_final", D), ("beta_final", D), ("timings_ms", D * 4),
+                ("boruvka_rounds", I64), ("exact_ties", I64), ("exact_rescans", I64)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "isoc_version": (ctypes.c_int, []),
@@ -66,6 +75,7 @@ SIGNATURES = {
     "isoc_witness": (ctypes.c_int, [P, I32, I64, P, P, P, P, PD]),
     "isoc_tree_destroy": (None, [P]),
     "isoc_exp_dev": (ctypes.c_int, [P, P, I64, P]),
+    "isoc_run": (ctypes.c_int, [P, I64, I32, I64, D, D, I64, P, ctypes.POINTER(RunOut)]),
     "isoc_launch_count": (ctypes.c_longlong, []),
     "isoc_prof_enable": (None, [ctypes.c_int]),
     "isoc_prof_read": (ctypes.c_int, [ctypes.c_int, PD, ctypes.POINTER(ctypes.c_longlong)]),
@@ -108,3 +118,36 @@ def check(status: int) -> None:
     if status == ISOC_ENOMEM:
         raise MemoryError(msg)
     raise RuntimeError(f"isoclust_b200: {msg}")
+
+
+def run(points, k: int, sigma: float = 0.0, alpha: float = 0.0, root: int = 0) -> dict:
+    """One-call C path (isoc_run): the whole pipeline on one GPU from host
+    numpy points; sigma <= 0 means "auto".  Returns the outputs as a dict."""
+    import numpy as np
+
+    X = np.ascontiguousarray(points, dtype=np.float64)
+    if X.ndim != 2:
+        raise ValueError(f"points must be a 2-d array, got shape {X.shape}")
+    if isinstance(k, bool) or not isinstance(k, (int, np.integer)):
+        raise TypeError(f"k must be an integer, got {type(k).__name__}")
+    n, d = X.shape
+    cap = 256
+    labels = np.empty(n, np.int64)
+    cut = np.empty(n, np.int8)
+    eta = np.empty(n, np.int64)
+    sp = np.empty(max(int(k), 1), np.float64)
+    tmid = np.empty(cap, np.float64)
+    tok = np.empty(cap, np.uint8)
+    out = RunOut()
+    out.labels, out.cut, out.eta = labels.ctypes.data, cut.ctypes.data, eta.ctypes.data
+    out.sparsities, out.trace_mid, out.trace_ok = sp.ctypes.data, tmid.ctypes.data, tok.ctypes.data
+    out.trace_cap = cap
+    check(load().isoc_run(X.ctypes.data, n, d, int(k), float(sigma), float(alpha), int(root), None,
+                          ctypes.byref(out)))
+    m = min(out.trace_len, cap)
+    return {"labels": labels, "cut": cut, "eta": eta, "sparsities": [float(v) for v in sp[:out.clusters_found]],
+            "trace": [(float(tmid[i]), bool(tok[i])) for i in range(m)], "iterations": int(out.iterations),
+            "miso": float(out.miso), "sigma": float(out.sigma), "alpha_final": float(out.alpha_final),
+            "beta_final": float(out.beta_final), "timings_ms": list(out.timings_ms),
+            "mst_stats": {"boruvka_rounds": int(out.boruvka_rounds), "exact_ties": int(out.exact_ties),
+                          "exact_rescans": int(out.exact_rescans)}}

@@ -46,6 +46,23 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
+}  // namespace
+
+namespace isoc {
+// error reporting for the host-side modules (run.cu)
+int set_error(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+}  // namespace isoc
+
+namespace {
+
 #define CK(expr)                                                                              \
     do {                                                                                      \
         cudaError_t _e = (expr);                                                              \
