@@ -1,11 +1,13 @@
 // K2s: symmetric omega pass with Boruvka round 2 fused (single GPU).
 //
 // Each unordered pair is computed once: CTA (I, J), I <= J, owns the
-// 1024 x 1024 super-tile of super-blocks I (rows) and J (columns) and walks
-// its 8 x 8 tiles of 128 x 128.  From every tile of flows
+// 1024 x 1024 super-tile of super-blocks I (rows) and J (columns).  Two
+// ping-pong teams of 256 threads each take 512 of the columns and walk their
+// 8 x 8 tiles of 128 x 64; their tile epilogues strictly alternate (named
+// barriers), so one team's FP64 loop always covers the other's epilogue.  From every tile of flows
 // f_ij = exp(-d_ij/sigma) (diagonal zeroed, vertex_weights,
 // /root/reference/pkg/src/isoclust/affinity.py:175-201) it folds
-//   rows i in I over the tile's columns  -> pow2 subtree sums, level 7, and
+//   rows i in I over the tile's columns  -> pow2 subtree sums, level 6, and
 //   columns j in J over the tile's rows  -> the transposed sums (d_ji == d_ij
 //                                           bitwise: scipy squares u-v)
 // and pushes them through per-row / per-column binary counters into complete
@@ -23,31 +25,38 @@
 namespace isoc {
 
 constexpr int SB = 1024;      // super-block
-constexpr int TBK = 128;      // tile
+constexpr int TBM = 128;      // tile rows
+constexpr int TBN = 64;       // tile columns
 constexpr int SK = 16;        // k chunk
-constexpr int STH = 512;      // threads
+constexpr int TEAM = 256;     // threads per team
+constexpr int STH = 2 * TEAM; // two ping-pong teams
+constexpr int HALF = SB / 2;  // columns per team
 
 struct SymStage {
-    double A[SK][TBK];
-    double B[SK][TBK];
+    double A[SK][TBM];
+    double B[SK][TBN];
+};
+
+struct TeamSmem {
+    SymStage st[2];
+    double rc[TBM][4];         // row counters over the team's 8 column tiles
+    double cc[HALF][4];        // column counters over the 8 row tiles
+    double xcol[8][TBN];       // column partials of the team's eight warps
+    double xcm[8][TBN];        // column-min exchange
+    int32_t xcj[8][TBN];
+    double rmin[TBM];
+    int32_t rminj[TBM];
+    double cmin[HALF];
+    int32_t cminj[HALF];
+    int32_t comp_r[TBM];       // component ids of the tile's rows / columns
+    int32_t comp_c[TBN];
 };
 
 struct SymSmem {
-    SymStage st[2];
-    double rc[TBK][4];         // row counters (3 levels used)
-    double cc[SB][4];          // column counters over row tiles
-    double xrow[2][TBK];       // row partials of the two column-half warps
-    double xcol[8][TBK];       // column partials of the eight row warps
-    double xrm[2][TBK];        // row-min exchange
-    int32_t xrj[2][TBK];
-    double xcm[8][TBK];        // column-min exchange
-    int32_t xcj[8][TBK];
-    double rmin[TBK];
-    int32_t rminj[TBK];
-    double cmin[SB];
-    int32_t cminj[SB];
-    int32_t comp_r[TBK];       // component ids of the tile's rows / columns
-    int32_t comp_c[TBK];
+    TeamSmem t[2];
+    double rowv[TBM];          // team 0's 512-column row subtrees / minima of the row tile
+    double rowm[TBM];
+    int32_t rowj[TBM];
     uint64_t exp_tab[256];     // exp table in shared memory (lane-divergent lookups)
 };
 
@@ -57,15 +66,18 @@ __device__ __forceinline__ void sym_cp16(void* dst, const void* src) {
 }
 
 __device__ __forceinline__ void sym_load(SymStage& s, const double* __restrict__ XT, int64_t np,
-                                         int64_t r0, int64_t c0, int kc) {
-    const int tid = threadIdx.x;
+                                         int64_t r0, int64_t c0, int kc, int ttid) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int q = ttid + TEAM * m;           // 0..1023 chunks of 16 B (A)
+        const int kk = q >> 6, part = q & 63;
+        sym_cp16(&s.A[kk][part * 2], XT + (int64_t)(kc * SK + kk) * np + r0 + part * 2);
+    }
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
-        const int q = tid + STH * m;            // 0..1023 chunks of 16 B
-        const int kk = q >> 6, part = q & 63;
-        const int64_t krow = (int64_t)(kc * SK + kk) * np;
-        sym_cp16(&s.A[kk][part * 2], XT + krow + r0 + part * 2);
-        sym_cp16(&s.B[kk][part * 2], XT + krow + c0 + part * 2);
+        const int q = ttid + TEAM * m;           // 0..511 chunks of 16 B (B)
+        const int kk = q >> 5, part = q & 31;
+        sym_cp16(&s.B[kk][part * 2], XT + (int64_t)(kc * SK + kk) * np + c0 + part * 2);
     }
 }
 
@@ -74,7 +86,8 @@ __device__ __forceinline__ bool lex_less(double a, int32_t ja, double b, int32_t
 }
 
 __device__ __forceinline__ double csum_push(double* slots, int idx, double v) {
-    // binary counter over 8 tiles (3 levels); returns v unchanged
+    // binary counter over the tiles; returns the value stored (the full
+    // subtree after the last push)
     int lvl = 0;
     int t = idx;
     while (t & 1) {
@@ -86,18 +99,31 @@ __device__ __forceinline__ double csum_push(double* slots, int idx, double v) {
     return v;
 }
 
+__device__ __forceinline__ void team_sync(int team) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "n"(TEAM) : "memory");
+}
+// epilogue tokens: team 0 waits on barrier 3, team 1 on barrier 4
+__device__ __forceinline__ void token_wait(int team) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(3 + team), "n"(STH) : "memory");
+}
+__device__ __forceinline__ void token_pass(int team) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(4 - team), "n"(STH) : "memory");
+}
+
 __global__ void __launch_bounds__(STH, 1)
 omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n, int64_t nbs,
                  double sigma, double rs, const int32_t* __restrict__ comp, double* __restrict__ PS,
                  double* __restrict__ PSm, int32_t* __restrict__ PSj) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SymSmem& sm = *reinterpret_cast<SymSmem*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int wr = w >> 1, wc = w & 1;
-    const int rg = wr * 4 + (lane >> 3), cl = lane & 7;
-    // thread columns (within the tile): wc*64 + 2*cl + 16*q + h, q < 4, h < 2
-    // -> the 8 lanes of a row group read 8 consecutive 16-byte chunks (no
-    //    bank conflicts); pairs (2p, 2p+1) are this thread's, p = cl + 8q
+    const int tid = threadIdx.x;
+    const int team = tid >> 8, ttid = tid & (TEAM - 1);
+    TeamSmem& ts = sm.t[team];
+    const int lane = tid & 31, w = ttid >> 5;
+    const int rg = ttid >> 3, cl = lane & 7;
+    // thread columns (within the tile): 2*cl + 16*q + h, q < 4, h < 2 -> the 8
+    // lanes of a row group read 8 consecutive 16-byte chunks (no bank
+    // conflicts); thread rows: 4*rg + i, i < 4
     // triangular decode of blockIdx -> (I, J), I <= J
     const int64_t b = blockIdx.x;
     int64_t J = (int64_t)((sqrt(8.0 * (double)b + 1.0) - 1.0) / 2.0);
@@ -105,47 +131,47 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
     while (J * (J + 1) / 2 > b) --J;
     const int64_t I = b - J * (J + 1) / 2;
     const bool diag = (I == J);
-    const int64_t R0 = I * SB, C0 = J * SB;
+    const int64_t R0 = I * SB, C0 = J * SB + team * HALF;   // this team's columns
     const int nk = dpad / SK;
     const bool want_min = comp != nullptr;
+    constexpr int TI = SB / TBM, TJ = HALF / TBN;   // 8 x 8 tiles per team
 
-    for (int e = tid; e < SB; e += STH) {
-        sm.cmin[e] = INFINITY;
-        sm.cminj[e] = INT32_MAX;
+    for (int e = ttid; e < HALF; e += TEAM) {
+        ts.cmin[e] = INFINITY;
+        ts.cminj[e] = INT32_MAX;
     }
     for (int e = tid; e < 256; e += STH) sm.exp_tab[e] = ISOC_EXP_TAB[e];
+    __syncthreads();
+    if (team == 1) token_pass(team);     // team 0 takes the first epilogue
     double acc[4][8];
     // linear pipeline over (ti, tj, kc)
-    const int total = 64 * nk;
-    sym_load(sm.st[0], XT, np, R0, C0, 0);
+    const int total = TI * TJ * nk;
+    sym_load(ts.st[0], XT, np, R0, C0, 0, ttid);
     asm volatile("cp.async.commit_group;\n" ::);
+    int kc = 0, tile = 0;
     for (int it = 0; it < total; ++it) {
-        const int tile = it / nk, kc = it % nk;
-        const int ti = tile >> 3, tj = tile & 7;
+        const int ti = tile / TJ, tj = tile % TJ;
         if (kc == 0) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-            if (tj == 0 && tid < TBK) {
-                sm.rmin[tid] = INFINITY;
-                sm.rminj[tid] = INT32_MAX;
+            if (want_min && ttid < TBM + TBN) {
+                const int64_t g = (ttid < TBM) ? R0 + ti * TBM + ttid : C0 + tj * TBN + (ttid - TBM);
+                const int32_t v = g < n ? comp[g] : (ttid < TBM ? -1 : -2);
+                if (ttid < TBM) ts.comp_r[ttid] = v; else ts.comp_c[ttid - TBM] = v;
             }
         }
-        if (kc == 0 && want_min && tid < 2 * TBK) {
-            const int64_t g = (tid < TBK) ? R0 + ti * TBK + tid : C0 + tj * TBK + (tid - TBK);
-            const int32_t v = g < n ? comp[g] : (tid < TBK ? -1 : -2);
-            if (tid < TBK) sm.comp_r[tid] = v; else sm.comp_c[tid - TBK] = v;
-        }
         if (it + 1 < total) {
-            const int t1 = (it + 1) / nk, k1 = (it + 1) % nk;
-            sym_load(sm.st[(it + 1) & 1], XT, np, R0 + (t1 >> 3) * TBK, C0 + (t1 & 7) * TBK, k1);
+            const int k1 = (kc + 1 == nk) ? 0 : kc + 1;
+            const int t1 = (kc + 1 == nk) ? tile + 1 : tile;
+            sym_load(ts.st[(it + 1) & 1], XT, np, R0 + (t1 / TJ) * TBM, C0 + (t1 % TJ) * TBN, k1, ttid);
         }
         asm volatile("cp.async.commit_group;\n" ::);
         asm volatile("cp.async.wait_group 1;\n" ::);
-        __syncthreads();
+        team_sync(team);
         {
-            const SymStage& s = sm.st[it & 1];
+            const SymStage& s = ts.st[it & 1];
 #pragma unroll 4
             for (int kk = 0; kk < SK; ++kk) {
                 const double2 a01 = *reinterpret_cast<const double2*>(&s.A[kk][rg * 4]);
@@ -154,7 +180,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 double bv[8];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const double2 t = *reinterpret_cast<const double2*>(&s.B[kk][wc * 64 + 2 * cl + 16 * q]);
+                    const double2 t = *reinterpret_cast<const double2*>(&s.B[kk][2 * cl + 16 * q]);
                     bv[2 * q] = t.x;
                     bv[2 * q + 1] = t.y;
                 }
@@ -164,28 +190,33 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                     for (int j = 0; j < 8; ++j) acc[i][j] = exact_sq_step(acc[i][j], a[i], bv[j]);
             }
         }
-        __syncthreads();
-        if (kc != nk - 1) continue;
+        team_sync(team);
+        if (++kc != nk) continue;
+        kc = 0;
+        ++tile;
 
         // ------------------------------------------------ tile epilogue
-        const int64_t gr0 = R0 + ti * TBK + rg * 4;   // first global row of this thread
-        const int64_t gcb = C0 + tj * TBK;             // first global col of the tile
-#define LCOL(j) (wc * 64 + 2 * cl + 16 * ((j) >> 1) + ((j) & 1))
+        // (the two teams' epilogues alternate; the other team's FP64 loop
+        // runs meanwhile)
+        token_wait(team);
+        const int64_t gr0 = R0 + ti * TBM + rg * 4;    // first global row of this thread
+        const int64_t gcb = C0 + tj * TBN;              // first global col of the tile
+#define LCOL(j) (2 * cl + 16 * ((j) >> 1) + ((j) & 1))
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[i][j] = __dsqrt_rn(acc[i][j]);
         if (want_min) {
-            // row minima (columns ascend within the thread; ties -> smaller column)
+            // row minima over the tile's 64 columns (ascending within the thread)
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int32_t cr = sm.comp_r[rg * 4 + i];
+                const int32_t cr = ts.comp_r[rg * 4 + i];
                 double m = INFINITY;
                 int32_t mj = INT32_MAX;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int64_t gi = gr0 + i, gj = gcb + LCOL(j);
-                    const bool ok = gi < n && gj < n && sm.comp_c[LCOL(j)] != cr;
+                    const bool ok = gi < n && gj < n && ts.comp_c[LCOL(j)] != cr;
                     if (ok && lex_less(acc[i][j], (int32_t)gj, m, mj)) { m = acc[i][j]; mj = (int32_t)gj; }
                 }
 #pragma unroll
@@ -194,19 +225,26 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                     const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
                     if (lex_less(om, oj, m, mj)) { m = om; mj = oj; }
                 }
-                if ((lane & 7) == 0) { sm.xrm[wc][rg * 4 + i] = m; sm.xrj[wc][rg * 4 + i] = mj; }
+                if (cl == 0) {
+                    const int r = rg * 4 + i;
+                    double pm = tj == 0 ? INFINITY : ts.rmin[r];
+                    int32_t pj = tj == 0 ? INT32_MAX : ts.rminj[r];
+                    if (lex_less(m, mj, pm, pj)) { pm = m; pj = mj; }
+                    ts.rmin[r] = pm;
+                    ts.rminj[r] = pj;
+                }
             }
-            // column minima (rows ascend within the thread)
+            // column minima over the thread's rows (ascending), then the warp
             if (!diag) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const int32_t cc = sm.comp_c[LCOL(j)];
+                    const int32_t cc = ts.comp_c[LCOL(j)];
                     double m = INFINITY;
                     int32_t mj = INT32_MAX;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int64_t gi = gr0 + i, gj = gcb + LCOL(j);
-                        const bool ok = gi < n && gj < n && sm.comp_r[rg * 4 + i] != cc;
+                        const bool ok = gi < n && gj < n && ts.comp_r[rg * 4 + i] != cc;
                         if (ok && acc[i][j] < m) { m = acc[i][j]; mj = (int32_t)gi; }
                     }
 #pragma unroll
@@ -215,7 +253,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                         const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
                         if (lex_less(om, oj, m, mj)) { m = om; mj = oj; }
                     }
-                    if ((lane >> 3) == 0) { sm.xcm[wr][LCOL(j)] = m; sm.xcj[wr][LCOL(j)] = mj; }
+                    if ((lane >> 3) == 0) { ts.xcm[w][LCOL(j)] = m; ts.xcj[w][LCOL(j)] = mj; }
                 }
             }
         }
@@ -228,9 +266,10 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 const bool valid = gi < n && gj < n && gi != gj;
                 acc[i][j] = valid ? isoc_flow_fast(acc[i][j], sigma, rs, sm.exp_tab) : 0.0;
             }
-        // row folds (pow2 tree over the tile's 128 columns): own pairs (level
+        // row folds (pow2 tree over the tile's 64 columns): own pairs (level
         // 1), lanes cl^1, cl^2, cl^4 (levels 2-4, one 16-column block per q),
-        // own q pairs (levels 5-6), then the two column halves (level 7)
+        // own q pairs (levels 5-6); 8 tiles -> the team's 512-column subtree;
+        // team 1 adds team 0's (left) subtree: the row's 1024-wide subtree
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             double v[4];
@@ -244,10 +283,31 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 y = __shfl_down_sync(0xffffffffu, x, 4);
                 v[q] = __dadd_rn(x, y);
             }
-            if (cl == 0)
-                sm.xrow[wc][rg * 4 + i] = __dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3]));
+            if (cl == 0) {
+                const int r = rg * 4 + i;
+                const double half = csum_push(ts.rc[r], tj, __dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3])));
+                if (tj == TJ - 1) {
+                    if (team == 0) {
+                        sm.rowv[r] = half;
+                        if (want_min) { sm.rowm[r] = ts.rmin[r]; sm.rowj[r] = ts.rminj[r]; }
+                    } else {
+                        const int64_t gi = R0 + ti * TBM + r;
+                        if (gi < n) {
+                            PS[J * n + gi] = __dadd_rn(sm.rowv[r], half);
+                            if (want_min) {
+                                double m = sm.rowm[r];
+                                int32_t mj = sm.rowj[r];
+                                if (lex_less(ts.rmin[r], ts.rminj[r], m, mj)) { m = ts.rmin[r]; mj = ts.rminj[r]; }
+                                PSm[J * n + gi] = m;
+                                PSj[J * n + gi] = mj;
+                            }
+                        }
+                    }
+                }
+            }
         }
-        // column folds: 4 own rows, then the 4 row groups of the warp
+        // column folds: 4 own rows, then the 4 row groups of the warp, then
+        // the team's 8 warps through shared memory
         if (!diag) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -255,53 +315,38 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 double y = __shfl_down_sync(0xffffffffu, x, 8);
                 if (((lane >> 3) & 1) == 0) x = __dadd_rn(x, y);
                 y = __shfl_down_sync(0xffffffffu, x, 16);
-                if ((lane >> 3) == 0) sm.xcol[wr][LCOL(j)] = __dadd_rn(x, y);
+                if ((lane >> 3) == 0) ts.xcol[w][LCOL(j)] = __dadd_rn(x, y);
             }
-        }
-        __syncthreads();
-        if (tid < TBK) {
-            const int r = tid;
-            const double full = csum_push(sm.rc[r], tj, __dadd_rn(sm.xrow[0][r], sm.xrow[1][r]));
-            if (want_min) {
-                double m = sm.rmin[r];
-                int32_t mj = sm.rminj[r];
-                for (int h = 0; h < 2; ++h)
-                    if (lex_less(sm.xrm[h][r], sm.xrj[h][r], m, mj)) { m = sm.xrm[h][r]; mj = sm.xrj[h][r]; }
-                sm.rmin[r] = m;
-                sm.rminj[r] = mj;
-            }
-            if (tj == 7) {
-                const int64_t gi = R0 + ti * TBK + r;
-                if (gi < n) {
-                    PS[J * n + gi] = full;   // 8 tiles = one complete 1024-wide subtree
-                    if (want_min) { PSm[J * n + gi] = sm.rmin[r]; PSj[J * n + gi] = sm.rminj[r]; }
+            team_sync(team);
+            if (ttid < TBN) {
+                const int c = ttid;
+                const double x01 = __dadd_rn(ts.xcol[0][c], ts.xcol[1][c]);
+                const double x23 = __dadd_rn(ts.xcol[2][c], ts.xcol[3][c]);
+                const double x45 = __dadd_rn(ts.xcol[4][c], ts.xcol[5][c]);
+                const double x67 = __dadd_rn(ts.xcol[6][c], ts.xcol[7][c]);
+                const int col = tj * TBN + c;
+                csum_push(ts.cc[col], ti, __dadd_rn(__dadd_rn(x01, x23), __dadd_rn(x45, x67)));
+                if (want_min) {
+                    double m = ts.cmin[col];
+                    int32_t mj = ts.cminj[col];
+                    for (int h = 0; h < 8; ++h)
+                        if (lex_less(ts.xcm[h][c], ts.xcj[h][c], m, mj)) { m = ts.xcm[h][c]; mj = ts.xcj[h][c]; }
+                    ts.cmin[col] = m;
+                    ts.cminj[col] = mj;
                 }
             }
-        } else if (!diag && tid < 2 * TBK) {
-            const int c = tid - TBK;
-            const double x01 = __dadd_rn(sm.xcol[0][c], sm.xcol[1][c]);
-            const double x23 = __dadd_rn(sm.xcol[2][c], sm.xcol[3][c]);
-            const double x45 = __dadd_rn(sm.xcol[4][c], sm.xcol[5][c]);
-            const double x67 = __dadd_rn(sm.xcol[6][c], sm.xcol[7][c]);
-            const int col = tj * TBK + c;
-            csum_push(sm.cc[col], ti, __dadd_rn(__dadd_rn(x01, x23), __dadd_rn(x45, x67)));
-            if (want_min) {
-                double m = sm.cmin[col];
-                int32_t mj = sm.cminj[col];
-                for (int h = 0; h < 8; ++h)
-                    if (lex_less(sm.xcm[h][c], sm.xcj[h][c], m, mj)) { m = sm.xcm[h][c]; mj = sm.xcj[h][c]; }
-                sm.cmin[col] = m;
-                sm.cminj[col] = mj;
-            }
+            team_sync(team);
         }
-        __syncthreads();
+        token_pass(team);
+#undef LCOL
     }
+    if (team == 0) token_wait(team);     // consume team 1's final hand-over
     if (!diag) {
-        for (int c = tid; c < SB; c += STH) {
+        for (int c = ttid; c < HALF; c += TEAM) {
             const int64_t gj = C0 + c;
             if (gj < n) {
-                PS[I * n + gj] = sm.cc[c][3];   // counter slot of the 8th row tile
-                if (want_min) { PSm[I * n + gj] = sm.cmin[c]; PSj[I * n + gj] = sm.cminj[c]; }
+                PS[I * n + gj] = ts.cc[c][3];   // counter slot of the 8th row tile
+                if (want_min) { PSm[I * n + gj] = ts.cmin[c]; PSj[I * n + gj] = ts.cminj[c]; }
             }
         }
     }
