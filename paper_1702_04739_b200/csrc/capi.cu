@@ -449,6 +449,12 @@ struct isoc_tree {
     int64_t spars_cap[2];
     int32_t *excl, *scratch;
     int64_t* j_out;
+    // batched speculative sweeps (isoc_decide_batch), allocated on first use
+    int32_t bcap;
+    double *bom, *bp, *bthr;
+    int8_t* bcode;
+    int32_t *bexcl, *bscratch;
+    int64_t* bj;
 };
 
 static void tree_free(isoc_tree* t) {
@@ -456,7 +462,8 @@ static void tree_free(isoc_tree* t) {
     void* ptrs[] = {t->bfs, t->pos_of, t->parent_v, t->depth_v, t->child_id_v, t->pos_parent,
                     t->child_lo, t->child_cnt, t->parent_d, t->flow_v, t->level_off, t->omega_v,
                     t->p_v, t->f_pos, t->om_pos, t->p_pos, t->om_w, t->p_w, t->code[0], t->code[1],
-                    t->spars[0], t->spars[1], t->excl, t->scratch, t->j_out};
+                    t->spars[0], t->spars[1], t->excl, t->scratch, t->j_out, t->bom, t->bp,
+                    t->bthr, t->bcode, t->bexcl, t->bscratch, t->bj};
     for (void* p : ptrs)
         if (p) cudaFreeAsync(p, t->st);
     delete t;
@@ -648,6 +655,48 @@ int isoc_decide(isoc_tree* t, double N, int64_t k, int32_t slot, int64_t* j_host
                      t->child_lo, t->child_cnt, N, k, t->om_w, t->p_w, t->code[slot], t->excl,
                      t->spars[slot], t->scratch, t->j_out, st));
     CK(cudaMemcpyAsync(j_host, t->j_out, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return ISOC_OK;
+}
+
+int isoc_tree_shape(isoc_tree* t, int64_t* levels, int64_t* max_width) {
+    if (!t) return fail(ISOC_EINVAL, "tree is NULL");
+    if (levels) *levels = t->levels;
+    if (max_width) *max_width = t->max_width;
+    return ISOC_OK;
+}
+
+int isoc_decide_batch(isoc_tree* t, const double* thresholds, int32_t count, int64_t k, int64_t* j_host) {
+    if (!t->omega_v) return fail(ISOC_EINVAL, "weights not attached");
+    if (k < 1) return fail(ISOC_EINVAL, "k must be >= 1, got %lld", (long long)k);
+    if (count < 1 || count > 16) return fail(ISOC_EINVAL, "batch of %d thresholds (1..16)", count);
+    for (int i = 0; i < count; ++i)
+        if (!std::isfinite(thresholds[i])) return fail(ISOC_EINVAL, "threshold must be finite, got %g", thresholds[i]);
+    cudaStream_t st = t->st;
+    const int64_t n = t->n;
+    if (t->bcap < count) {
+        void* old[] = {t->bom, t->bp, t->bthr, t->bcode, t->bexcl, t->bscratch, t->bj};
+        for (void* q : old)
+            if (q) cudaFreeAsync(q, st);
+        t->bom = t->bp = t->bthr = nullptr;
+        t->bcode = nullptr;
+        t->bexcl = t->bscratch = nullptr;
+        t->bj = nullptr;
+        t->bcap = 0;
+        CK(dalloc(&t->bom, (size_t)count * n, st));
+        CK(dalloc(&t->bp, (size_t)count * n, st));
+        CK(dalloc(&t->bcode, (size_t)count * n, st));
+        CK(dalloc(&t->bexcl, (size_t)count * n, st));
+        CK(dalloc(&t->bscratch, 16 * 1024 + 8, st));
+        CK(dalloc(&t->bthr, 16, st));
+        CK(dalloc(&t->bj, 16, st));
+        t->bcap = count;
+    }
+    CK(cudaMemcpyAsync(t->bthr, thresholds, (size_t)count * 8, cudaMemcpyHostToDevice, st));
+    CK(launch_decide_batch(n, t->levels, t->level_off, t->max_width, t->f_pos, t->om_pos, t->p_pos,
+                           t->child_lo, t->child_cnt, t->bthr, count, k, t->bom, t->bp, t->bcode,
+                           t->bexcl, t->bscratch, t->bj, st));
+    CK(cudaMemcpyAsync(j_host, t->bj, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return ISOC_OK;
 }

@@ -163,6 +163,190 @@ __global__ void __launch_bounds__(512) decide_kernel(DecideArgs A) {
     if (b == 0 && tid == 0) *A.j_out = j;
 }
 
+// Batched decision sweeps: K thresholds share one level-synchronous pass
+// (the speculative bisection of SURVEY 8f: the 2^m - 1 thresholds the next m
+// bisection steps could visit).  Same per-instance arithmetic as
+// decide_kernel; only the feasibility count j per threshold is returned (the
+// witness of the chosen threshold is re-derived by one decide_kernel sweep).
+constexpr int DB_MAX = 16;
+
+struct DecideBatchArgs {
+    int64_t n;
+    int64_t levels;
+    const int64_t* level_off;
+    const double* f_pos;
+    const double* om0;
+    const double* p0;
+    const int32_t* child_lo;
+    const int32_t* child_cnt;
+    const double* thr;   // K thresholds (device)
+    int K;
+    int64_t k;
+    double* om;          // [K][n]
+    double* p;           // [K][n]
+    int8_t* code;        // [K][n]
+    int32_t* excl;       // [K][n]
+    int32_t* chunk_cnt;  // [K][gridDim.x]
+    int64_t* j_out;      // [K]
+    unsigned int* bar;
+};
+
+__global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
+    // instance kk = blockIdx.x / Gi runs on its own Gi CTAs (local index bi);
+    // all CTAs share the grid barriers
+    __shared__ int32_t warp_tot[16];
+    __shared__ int64_t s_off, s_tot;
+    __shared__ int s_all_done;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int K = A.K;
+    const int Gi = gridDim.x / K;
+    const int kk = blockIdx.x / Gi, bi = blockIdx.x % Gi;
+    const int64_t n = A.n;
+    const double thr = A.thr[kk];
+    double* om = A.om + kk * n;
+    double* pp = A.p + kk * n;
+    int8_t* code = A.code + kk * n;
+    int32_t* excl = A.excl + kk * n;
+    int32_t* chunk_cnt = A.chunk_cnt + kk * Gi;
+    for (int64_t q = (int64_t)bi * blockDim.x + tid; q < n; q += (int64_t)Gi * blockDim.x) {
+        om[q] = A.om0[q];
+        pp[q] = A.p0[q];
+        code[q] = 0;
+    }
+    grid_barrier(A.bar);
+    int64_t j = 0;
+    for (int64_t lv = A.levels - 1; lv >= 0; --lv) {
+        const int64_t lo = A.level_off[lv], hi = A.level_off[lv + 1];
+        const int64_t W = hi - lo;
+        const int64_t cb = W * bi / Gi, ce = W * (bi + 1) / Gi;
+        const bool active = j < A.k;
+        int64_t carry = 0;
+        if (active) {
+            for (int64_t base = cb; base < ce; base += blockDim.x) {
+                const int64_t c = base + tid;
+                int32_t is_cut = 0;
+                if (c < ce) {
+                    const int64_t pos = hi - 1 - c;
+                    const double f = A.f_pos[pos], pw = pp[pos], ow = om[pos];
+                    const double rhs = __dmul_rn(thr, ow);
+                    int8_t cond;
+                    if (__dadd_rn(f, pw) <= rhs) cond = 1;
+                    else if (__dsub_rn(pw, f) < rhs) cond = 2;
+                    else cond = 3;
+                    is_cut = cond == 1;
+                    code[pos] = cond;
+                }
+                int32_t x = is_cut;
+                for (int o = 1; o < 32; o <<= 1) {
+                    int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (lane == 31) warp_tot[wid] = x;
+                __syncthreads();
+                if (wid == 0) {
+                    int32_t t = lane < nw ? warp_tot[lane] : 0;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                        if (lane >= o) t += y;
+                    }
+                    if (lane < nw) warp_tot[lane] = t;
+                }
+                __syncthreads();
+                const int32_t wpre = wid > 0 ? warp_tot[wid - 1] : 0;
+                if (c < ce) excl[hi - 1 - c] = (int32_t)(carry + wpre + x - is_cut);
+                carry += warp_tot[nw - 1];
+                __syncthreads();
+            }
+        }
+        if (tid == 0) chunk_cnt[bi] = (int32_t)carry;
+        grid_barrier(A.bar);
+        if (tid == 0) {
+            int64_t pre = 0, tot = 0;
+            for (int q = 0; q < Gi; ++q) {
+                const int64_t s = chunk_cnt[q];
+                if (q < bi) pre += s;
+                tot += s;
+            }
+            s_off = pre;
+            s_tot = tot;
+        }
+        __syncthreads();
+        const int64_t need = A.k - j;
+        const int64_t off = s_off, tot = s_tot;
+        if (active)
+            for (int64_t c = cb + tid; c < ce; c += blockDim.x) {
+                const int64_t pos = hi - 1 - c;
+                if (off + excl[pos] >= need) code[pos] = 0;
+            }
+        grid_barrier(A.bar);
+        if (lv > 0 && active) {
+            const int64_t plo = A.level_off[lv - 1], phi = lo;
+            const int64_t PW = phi - plo;
+            for (int64_t u = plo + (PW * bi) / Gi + tid; u < plo + (PW * (bi + 1)) / Gi; u += blockDim.x) {
+                const int32_t clo = A.child_lo[u], cnt = A.child_cnt[u];
+                double pu = pp[u], ou = om[u];
+                bool touched = false;
+                for (int32_t q = clo + cnt - 1; q >= clo; --q) {
+                    const int8_t cd = code[q];
+                    if (cd == 1 || cd == 3) {
+                        pu = __dadd_rn(pu, A.f_pos[q]);
+                        touched = true;
+                    } else if (cd == 2) {
+                        ou = __dadd_rn(ou, om[q]);
+                        pu = __dadd_rn(pu, pp[q]);
+                        touched = true;
+                    }
+                }
+                if (touched) {
+                    pp[u] = pu;
+                    om[u] = ou;
+                }
+            }
+        }
+        if (active) j += (tot < need) ? tot : need;
+        // instances publish whether they are done; stop when all are
+        if (bi == 0 && tid == 0) A.j_out[kk] = j;
+        grid_barrier(A.bar);
+        if (tid == 0) {
+            int done = 1;
+            for (int q = 0; q < K; ++q) done &= (((volatile int64_t*)A.j_out)[q] >= A.k);
+            s_all_done = done;
+        }
+        __syncthreads();
+        if (s_all_done) break;
+    }
+    if (bi == 0 && tid == 0) A.j_out[kk] = j;
+}
+
+cudaError_t launch_decide_batch(int64_t n, int64_t levels, const int64_t* level_off, int64_t max_width,
+                                const double* f_pos, const double* om0, const double* p0,
+                                const int32_t* child_lo, const int32_t* child_cnt, const double* thr,
+                                int K, int64_t k, double* om, double* p, int8_t* code, int32_t* excl,
+                                int32_t* scratch, int64_t* j_out, cudaStream_t st) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decide_batch_kernel, 512, 0);
+    const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    int64_t gi = (max_width + 8191) / 8192;
+    if (gi < 1) gi = 1;
+    if (gi * K > cap) gi = cap / K > 0 ? cap / K : 1;
+    const int G = (int)(gi * K);
+    DecideBatchArgs A;
+    A.n = n; A.levels = levels; A.level_off = level_off; A.f_pos = f_pos; A.om0 = om0; A.p0 = p0;
+    A.child_lo = child_lo; A.child_cnt = child_cnt; A.thr = thr; A.K = K; A.k = k; A.om = om; A.p = p;
+    A.code = code; A.excl = excl; A.chunk_cnt = scratch; A.j_out = j_out;
+    A.bar = reinterpret_cast<unsigned int*>(scratch + DB_MAX * 1024);
+    cudaMemsetAsync(A.bar, 0, 2 * sizeof(unsigned int), st);
+    cudaMemsetAsync(j_out, 0, (size_t)K * sizeof(int64_t), st);
+    void* args[] = {&A};
+    const int pid = prof_begin(PK_DECIDE, st);
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)decide_batch_kernel, dim3(G), dim3(512), args, 0, st);
+    prof_end(pid, st);
+    note_launch();
+    return e;
+}
+
 int decide_grid_size(int64_t max_width) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);

@@ -102,6 +102,11 @@ cudaError_t launch_extrema(const double* flow_v, int64_t root, const double* ome
                            cudaStream_t st);
 
 // decide.cu
+cudaError_t launch_decide_batch(int64_t n, int64_t levels, const int64_t* level_off, int64_t max_width,
+                                const double* f_pos, const double* om0, const double* p0,
+                                const int32_t* child_lo, const int32_t* child_cnt, const double* thr,
+                                int K, int64_t k, double* om, double* p, int8_t* code, int32_t* excl,
+                                int32_t* scratch, int64_t* j_out, cudaStream_t st);
 cudaError_t launch_decide(int64_t n, int64_t levels, const int64_t* level_off, int64_t max_width,
                           const double* f_pos, const double* om0, const double* p0,
                           const int32_t* child_lo, const int32_t* child_cnt, double thr, int64_t k,

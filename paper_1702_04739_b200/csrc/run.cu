@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
 
@@ -226,21 +227,97 @@ int run_impl(const double* points, int64_t n, int32_t d, int64_t k, double sigma
         ok = (j == k);
         return ISOC_OK;
     };
-    for (int64_t r = 0; r < t_budget; ++r) {
-        if (hi - lo <= 1e-15 * (1.0 > hi ? 1.0 : hi)) break;
-        const double mid = (lo + hi) / 2.0;
-        bool ok;
-        int64_t j;
-        int slot;
-        RCK(sweep(mid, ok, j, slot));
-        ++iters;
-        record(mid, ok);
-        if (ok) {
-            hi = mid;
-            wslot = slot;
-            wj = j;
-        } else {
-            lo = mid;
+    auto stop_test = [](double a, double b) { return b - a <= 1e-15 * (1.0 > b ? 1.0 : b); };
+    // speculation depth: as pipeline._speculation_depth (ISOC_SPEC_M overrides)
+    int m = 1;
+    {
+        int64_t levels = 1, width = 0;
+        RCK(isoc_tree_shape(tree, &levels, &width));
+        m = (n <= 64 * 1024 * (levels > 1 ? levels : 1) && width <= 262144) ? 4 : 1;
+        if (const char* e = getenv("ISOC_SPEC_M")) {
+            m = atoi(e);
+            m = m < 1 ? 1 : (m > 4 ? 4 : m);
+        }
+    }
+    if (m <= 1) {
+        for (int64_t r = 0; r < t_budget; ++r) {
+            if (stop_test(lo, hi)) break;
+            const double mid = (lo + hi) / 2.0;
+            bool ok;
+            int64_t j;
+            int slot;
+            RCK(sweep(mid, ok, j, slot));
+            ++iters;
+            record(mid, ok);
+            if (ok) {
+                hi = mid;
+                wslot = slot;
+                wj = j;
+            } else {
+                lo = mid;
+            }
+        }
+    } else {
+        // speculative bisection: see pipeline.run_bisection
+        bool have_w = false, stop = false;
+        double wthr = 0.0;
+        while (!stop && iters < t_budget) {
+            double thr[16];
+            int kid[16][2];
+            int cnt = 0;
+            const int64_t depth = (m < t_budget - iters) ? m : (t_budget - iters);
+            // iterative build in the same preorder as the Python recursion
+            struct Frame { double a, b; int depth, parent, side; };
+            Frame stk[64];
+            int sp = 0;
+            stk[sp++] = {lo, hi, (int)depth, -1, 0};
+            int root = -1;
+            while (sp > 0) {
+                const Frame f = stk[--sp];
+                int idx = -1;
+                if (f.depth > 0 && !stop_test(f.a, f.b)) {
+                    const double mid = (f.a + f.b) / 2.0;
+                    idx = cnt++;
+                    thr[idx] = mid;
+                    kid[idx][0] = kid[idx][1] = -1;
+                    // push right first so the left subtree is built first (preorder)
+                    stk[sp++] = {mid, f.b, f.depth - 1, idx, 1};
+                    stk[sp++] = {f.a, mid, f.depth - 1, idx, 0};
+                }
+                if (f.parent < 0) root = idx;
+                else kid[f.parent][f.side] = idx;
+            }
+            if (root < 0) break;
+            int64_t js[16];
+            RCK(isoc_decide_batch(tree, thr, cnt, k, js));
+            int node = root;
+            while (node >= 0) {
+                if (stop_test(lo, hi)) {
+                    stop = true;
+                    break;
+                }
+                const double mid = thr[node];
+                const bool ok = js[node] == k;
+                ++iters;
+                record(mid, ok);
+                if (ok) {
+                    hi = mid;
+                    wthr = mid;
+                    wj = js[node];
+                    have_w = true;
+                    node = kid[node][0];
+                } else {
+                    lo = mid;
+                    node = kid[node][1];
+                }
+                if (iters >= t_budget) break;
+            }
+        }
+        if (have_w) {
+            int64_t j = 0;
+            RCK(isoc_decide(tree, wthr, k, 0, &j));
+            if (j != wj) return isoc::set_error(ISOC_ECUDA, "speculative sweep disagrees with the witness sweep");
+            wslot = 0;
         }
     }
     if (wslot < 0) {

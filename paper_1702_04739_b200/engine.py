@@ -252,6 +252,18 @@ class DeviceTree:
         check(self.b.lib.isoc_decide(self.h, float(N), int(k), int(slot), ctypes.byref(j)))
         return int(j.value)
 
+    def decide_batch(self, thresholds, k: int) -> list:
+        """Cut counts j at up to 16 thresholds in one level-synchronous pass."""
+        thr = np.ascontiguousarray(thresholds, dtype=np.float64)
+        j = np.empty(thr.shape[0], np.int64)
+        check(self.b.lib.isoc_decide_batch(self.h, thr.ctypes.data, int(thr.shape[0]), int(k), j.ctypes.data))
+        return [int(v) for v in j]
+
+    def shape(self) -> tuple:
+        lv, mw = ctypes.c_int64(), ctypes.c_int64()
+        check(self.b.lib.isoc_tree_shape(self.h, ctypes.byref(lv), ctypes.byref(mw)))
+        return int(lv.value), int(mw.value)
+
     def witness(self, slot: int, k: int) -> Witness:
         n = self.n
         labels = np.empty(n, np.int64)

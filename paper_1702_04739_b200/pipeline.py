@@ -331,6 +331,19 @@ def decide(tree: RootedTree, weights: NodeWeights, k: int, N: float) -> Decision
 par_decide = decide
 
 
+def _speculation_depth(dt: DeviceTree) -> int:
+    """Bisection steps per batched sweep: 4 (15 thresholds) on latency-bound
+    trees whose levels are narrow (MST trees of C1-C4), 1 (plain sequential
+    sweeps) on wide, HBM-bound trees (C5).  ISOC_SPEC_M overrides."""
+    env = os.environ.get("ISOC_SPEC_M")
+    if env is not None:
+        return max(1, min(4, int(env)))
+    if not hasattr(dt, "shape"):
+        return 1
+    levels, width = dt.shape()
+    return 4 if dt.n <= 64 * 1024 * max(1, levels) and width <= 262144 else 1
+
+
 def run_bisection(dt: DeviceTree, ext: Extrema, k: int, n: int) -> MisoResult:
     """isoperim.py:222-308 with device decision sweeps.
 
@@ -363,18 +376,70 @@ def run_bisection(dt: DeviceTree, ext: Extrema, k: int, n: int) -> MisoResult:
         j = dt.decide(N, k, slot)
         return j == k, j, slot
 
-    for _ in range(t):
-        if beta - alpha <= BRACKET_EPS * max(1.0, beta):
-            break
-        mid = (alpha + beta) / 2.0
-        ok, j, slot = sweep(mid)
-        rounds += 1
-        trace.append((mid, ok))
-        if ok:
-            beta = mid
-            wslot, wj = slot, j
-        else:
-            alpha = mid
+    m = _speculation_depth(dt)
+    if m <= 1:
+        for _ in range(t):
+            if beta - alpha <= BRACKET_EPS * max(1.0, beta):
+                break
+            mid = (alpha + beta) / 2.0
+            ok, j, slot = sweep(mid)
+            rounds += 1
+            trace.append((mid, ok))
+            if ok:
+                beta = mid
+                wslot, wj = slot, j
+            else:
+                alpha = mid
+    else:
+        # Speculative bisection: the thresholds the next m steps
+        # can visit, built with the reference's own float recursion and stop
+        # test, are swept in one batched pass; the walk then replays the
+        # sequential loop on their outcomes.  The witness is re-derived at the
+        # last feasible midpoint by one ordinary sweep.
+        wthr = None
+        stop = False
+        while not stop and rounds < t:
+            thr: list = []
+            kids: list = []
+
+            def build(a: float, b: float, depth: int) -> int:
+                if depth == 0 or b - a <= BRACKET_EPS * max(1.0, b):
+                    return -1
+                mid = (a + b) / 2.0
+                idx = len(thr)
+                thr.append(mid)
+                kids.append(None)
+                kids[idx] = (build(a, mid, depth - 1), build(mid, b, depth - 1))
+                return idx
+
+            root = build(alpha, beta, min(m, t - rounds))
+            if root < 0:
+                break
+            js = dt.decide_batch(thr, k)
+            node = root
+            while node >= 0:
+                if beta - alpha <= BRACKET_EPS * max(1.0, beta):
+                    stop = True
+                    break
+                mid = thr[node]
+                j = js[node]
+                ok = j == k
+                rounds += 1
+                trace.append((mid, ok))
+                if ok:
+                    beta = mid
+                    wthr, wj = mid, j
+                    node = kids[node][0]
+                else:
+                    alpha = mid
+                    node = kids[node][1]
+                if rounds >= t:
+                    break
+        if wthr is not None:
+            j = dt.decide(wthr, k, 0)
+            if j != wj:
+                raise RuntimeError(f"speculative sweep disagrees with the witness sweep ({j} != {wj})")
+            wslot = 0
 
     if wslot is None:
         ok, j, slot = sweep(beta0)
