@@ -200,14 +200,28 @@ def tree_phase_bench(args):
         ext = pkg.extrema(tree, w)
         return pkg.par_solve_miso(tree, w, ext, k)
 
+    from paper_1702_04739_b200 import _lib
+    import ctypes
+
+    lib = _lib.load()
+    lib.isoc_prof_read.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                   ctypes.POINTER(ctypes.c_longlong)]
     for _ in range(args.warmup):
         res = step()
     torch.cuda.synchronize()
+    lib.isoc_prof_enable(1)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         res = step()
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
+    kernels = {}
+    for kind, name in enumerate(KIND_NAMES):
+        tot = ctypes.c_double()
+        cnt = ctypes.c_longlong()
+        if lib.isoc_prof_read(kind, ctypes.byref(tot), ctypes.byref(cnt)) == 0 and cnt.value:
+            kernels[name] = {"ms_total": tot.value / args.steps, "launches": cnt.value / args.steps}
+    lib.isoc_prof_enable(0)
     print(json.dumps({
         "metric": "tree-phase vertices/sec (C5: random spanning tree, 50M vertices, k=100)",
         "value": n * args.steps / el, "unit": "vertices/s", "n_gpus": 1, "steps": args.steps,
@@ -215,7 +229,7 @@ def tree_phase_bench(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic random recursive tree (PCG64 seed 0), flows 1-U, omega 2-1.9U, p=0",
         "config": {"workload": f"c5 tree phase N={n} k={k}", "n": n, "k": k},
-        "iterations": res.iterations, "miso": res.miso,
+        "iterations": res.iterations, "miso": res.miso, "kernels": kernels,
         "e2e": {"value": n * args.steps / el, "unit": "vertices/s",
                 "h2d_bytes_per_step": n * 24, "d2h_bytes_per_step": n * 17}}), flush=True)
 
