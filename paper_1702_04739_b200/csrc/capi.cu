@@ -177,9 +177,25 @@ int isoc_sigma_partial(const double* X, int64_t n, int32_t d, int64_t lo, int64_
     CK(cudaMemsetAsync(sown, 0, rows, st));
     if (sigma_sym_applicable(n, lo, hi, want_p))
         CK(launch_sigma_sym(X, n, d, row_vals, row_ids, row_cnt, flags, nn_j, nn_d, nn_tie, st));
-    else
-        CK(launch_sigma_pass(X, n, d, lo, hi, want_p, row_vals, row_ids, row_cnt, flags, nn_j, nn_d,
-                             nn_tie, want_p ? p_dev : nullptr, st));
+    else {
+        // the row pass always evaluates the nearest neighbours; give it scratch
+        // when the caller does not want them
+        int32_t* tj = nn_j;
+        double* td = nn_d;
+        int8_t* tt = nn_tie;
+        if (!nn_j) {
+            CK(aalloc(&tj, rows, st));
+            CK(aalloc(&td, rows, st));
+            CK(aalloc(&tt, rows, st));
+        }
+        CK(launch_sigma_pass(X, n, d, lo, hi, want_p, row_vals, row_ids, row_cnt, flags, tj, td, tt,
+                             want_p ? p_dev : nullptr, st));
+        if (!nn_j) {
+            cudaFreeAsync(tj, st);
+            cudaFreeAsync(td, st);
+            cudaFreeAsync(tt, st);
+        }
+    }
     const int64_t b_hi = hi + 1;  // boundaries lo+1 .. hi (boundary n = the final leaf)
     CK(launch_sigma_straddle(X, n, d, lo + 1, b_hi, sval, sid, sown, st));
     CK(launch_sigma_merge_rows(n, lo, hi, 64, row_vals, row_ids, row_cnt, sval, sid, sown, groups,

@@ -108,17 +108,21 @@ class CudaBackend:
         return self.torch.empty(shape, dtype=dtype, device=self.device)
 
     # -- exact passes -------------------------------------------------
-    def sigma_partial(self, X, n: int, d: int, lo: int, hi: int, alpha: float):
+    def sigma_partial(self, X, n: int, d: int, lo: int, hi: int, alpha: float, want_nn: bool = True):
         torch = self.torch
         rows = hi - lo
         stack = self.empty((_lib.FOLD_STACK_BYTES,), torch.uint8)
-        nn_j = self.empty((rows,), torch.int32)
-        nn_d = self.empty((rows,), torch.float64)
-        nn_tie = self.empty((rows,), torch.int8)
         p = self.empty((rows,), torch.float64)
-        check(self.lib.isoc_sigma_partial(_ptr(X), n, d, lo, hi, float(alpha), _ptr(stack),
-                                          _ptr(nn_j), _ptr(nn_d), _ptr(nn_tie), _ptr(p), self.stream))
-        return stack, (nn_j, nn_d, nn_tie), p
+        if want_nn:
+            nn_j = self.empty((rows,), torch.int32)
+            nn_d = self.empty((rows,), torch.float64)
+            nn_tie = self.empty((rows,), torch.int8)
+            ptrs = (_ptr(nn_j), _ptr(nn_d), _ptr(nn_tie))
+        else:
+            ptrs = (None, None, None)
+        check(self.lib.isoc_sigma_partial(_ptr(X), n, d, lo, hi, float(alpha), _ptr(stack), *ptrs, _ptr(p),
+                                          self.stream))
+        return stack, ((nn_j, nn_d, nn_tie) if want_nn else None), p
 
     def sigma_finish(self, stacks) -> float:
         total = ctypes.c_double(0.0)

@@ -133,9 +133,18 @@ class _Points:
         self.lo, self.hi = self.comm.rows(self.n)
 
 
-def _sigma_pass(P: _Points, alpha: float):
-    stack, nn, p_loc = P.b.sigma_partial(P.X, P.n, P.d, P.lo, P.hi, alpha)
-    return stack, nn, p_loc
+def _sigma_pass(P: _Points, alpha: float, want_nn: bool = True):
+    if want_nn:
+        return P.b.sigma_partial(P.X, P.n, P.d, P.lo, P.hi, alpha)
+    return P.b.sigma_partial(P.X, P.n, P.d, P.lo, P.hi, alpha, want_nn=False)
+
+
+def _round1_from_sigma(P: _Points) -> bool:
+    """Borůvka round 1 from the sigma pass's exact nearest neighbours (default)
+    or from the tensor-core filter (ISOC_ROUND1=filter: the symmetric sigma
+    pass then skips the neighbour bookkeeping, ~6% of it, but singletons
+    leave many uncertified rows to rescan -- a wash at n = 400k)."""
+    return os.environ.get("ISOC_ROUND1", "nn") != "filter"
 
 
 def _sigma_from_stack(P: _Points, stack) -> float:
@@ -508,7 +517,7 @@ def run_pipeline(
     nn = None
     p_loc = None
     if need_pass:
-        stack, nn, p_loc = _sigma_pass(P, float(alpha) if alpha > 0 else 0.0)
+        stack, nn, p_loc = _sigma_pass(P, float(alpha) if alpha > 0 else 0.0, _round1_from_sigma(P))
         sigma_val = _sigma_from_stack(P, stack) if sigma == "auto" else float(sigma)
     else:
         sigma_val = float(sigma)

@@ -105,7 +105,7 @@ class EmuBackend:
 
     # K1 restated per shard: row stacks, straddle leaves, merge (the CUDA
     # algorithm of exact_passes.cu, in Python)
-    def sigma_partial(self, X, n, d, lo, hi, alpha):
+    def sigma_partial(self, X, n, d, lo, hi, alpha, want_nn=True):
         Xn = X.numpy()
         total = n * n
         rows = orc.distance_rows(Xn, lo, hi)
@@ -138,8 +138,8 @@ class EmuBackend:
             nn_tie[i - lo] = int(r2.min() == r[j])
         self._straddle(Xn, n, total, hi, st)
         p = np.zeros(hi - lo) if alpha == 0 else orc.row_folds(Xn, 1.0, alpha, lo, hi)[1]
-        return pack_stack(st), (torch.from_numpy(nn_j), torch.from_numpy(nn_d),
-                                torch.from_numpy(nn_tie)), torch.from_numpy(p)
+        nn = (torch.from_numpy(nn_j), torch.from_numpy(nn_d), torch.from_numpy(nn_tie)) if want_nn else None
+        return pack_stack(st), nn, torch.from_numpy(p)
 
     @staticmethod
     def _straddle(Xn, n, total, b, st):
