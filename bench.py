@@ -340,12 +340,12 @@ def main():
     rounds = run.mst_stats.get("boruvka_rounds", 0)
     # algorithmic flops per launch: exact passes 3*d fp64 flops per
     # ordered pair over all n^2 pairs; the FP32 filter 2*d per pair it scans
-    use_tc = d <= 64 and os.environ.get("ISOC_FILTER", "") != "ffma"
+    use_tc = d <= 512 and os.environ.get("ISOC_FILTER", "") != "ffma"
     alg = {
         "sigma_pass": 3.0 * d * n * n,
         "omega_pass": 3.0 * d * n * n,
-        # tcgen05 filter: 3 FP16 MMA passes (hi.hi, hi.lo, lo.hi) over K = 64 per pair
-        "boruvka_filter": (3 * 2.0 * 64 if use_tc else 2.0 * d) * n * n,
+        # tcgen05 filter: 3 FP16 MMA passes (hi.hi, hi.lo, lo.hi) over K = 64 per atom per pair
+        "boruvka_filter": (3 * 2.0 * 64 * ((d + 63) // 64) if use_tc else 2.0 * d) * n * n,
     }
     # the exact passes' fp64 ops cannot fuse (scipy's separately rounded
     # mul/add), so their ceiling is the DADD/DMUL issue rate = half the

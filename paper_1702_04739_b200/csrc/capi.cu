@@ -325,7 +325,7 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
     MCK(launch_prep_fp32(X, n, d, h->dp, h->npad, h->centre, h->Y, h->ny, h->rad, h->rmax, h->st));
     // tensor-core filter (tcgen05, 3-term FP16 split) for d <= 64 unless ISOC_FILTER=ffma
     const char* fenv = getenv("ISOC_FILTER");
-    h->use_tc = (d <= 64) && !(fenv && strcmp(fenv, "ffma") == 0);
+    h->use_tc = (d <= 512) && !(fenv && strcmp(fenv, "ffma") == 0);
     if (h->use_tc) {
         uint32_t* am = nullptr;
         MCK(dalloc(&am, 1, h->st));
@@ -343,9 +343,11 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
         const float scale = (float)ldexp(1.0, s);
         h->kscale = (float)-ldexp(1.0, 1 - 2 * s);
         // split + tensor-core accumulation bound ("filter bound")
-        h->cd = (float)(((13.0 * 64 + 40.0) * 0x1p-24 + 0x1p-30) * 1.25);
-        h->cabs = (float)(ldexp(1.0, -22 - s) * 8.0 * 2.0);
-        MCK(dalloc(&h->img, tc_image_bytes(n), h->st));
+        // (linear in the padded depth, as the FFMA bound; 64 per K atom)
+        const double kd = (double)((d + 63) / 64 * 64);
+        h->cd = (float)(((13.0 * kd + 40.0) * 0x1p-24 + 0x1p-30) * 1.25);
+        h->cabs = (float)(ldexp(1.0, -22 - s) * 8.0 * 2.0 * (kd / 64.0));
+        MCK(dalloc(&h->img, tc_image_bytes(n, d), h->st));
         MCK(launch_tc_image(h->Y, h->npad, d, scale, n, h->img, h->st));
     } else {
         h->cabs = 0.f;
@@ -363,7 +365,7 @@ int isoc_mst_round_local(isoc_mst* h, int use_nn, const int32_t* nn_j, const dou
                                 h->cand_tie, st));
     } else {
         if (h->use_tc)
-            CK(launch_filter_tc(h->img, h->ny, h->comp, h->n, h->lo, h->hi, h->kscale, h->a1, h->j1, h->a2,
+            CK(launch_filter_tc(h->img, h->ny, h->comp, h->n, h->d, h->lo, h->hi, h->kscale, h->a1, h->j1, h->a2,
                                 st));
         else
             CK(launch_boruvka_filter(h->Y, h->ny, h->comp, h->n, h->npad, h->dp, h->lo, h->hi, h->a1,

@@ -15,8 +15,9 @@
 // (one elected lane); warps 2-9: epilogue, one thread per row reading its
 // 128 accumulator columns with tcgen05.ld and keeping (a1, j1, a2).
 // Accumulators are double buffered in TMEM (2 x 256 columns) so the MMA of
-// tile t+1 overlaps the epilogue of tile t.  d <= 64 (one 64-wide K atom);
-// larger d uses the FFMA kernel.
+// tile t+1 overlaps the epilogue of tile t.  d <= 64: one 64-wide K atom,
+// A resident; d > 64: every stage streams one K atom of A (both row blocks)
+// and of the tile, accumulating the atoms in TMEM.
 #include <cstdint>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -36,7 +37,10 @@ constexpr int TC_PART = 16384;      // bytes of one 128 x 64 fp16 image
 constexpr int TC_META = 8;
 constexpr int TC_MS = 4;            // metadata ring slots
 
-struct TcSmem {
+// Resident-A layout (d <= 64: one 64-wide K atom) and streaming layout
+// (d > 64: each stage carries one K atom of both row blocks and the tile).
+template <bool STREAM>
+struct TcSmemT {
     uint8_t A[2][2][TC_PART];            // [row block][hi/lo]
     uint8_t B[TC_STAGES][2][TC_PART];    // [stage][hi/lo]
     int32_t mcomp[TC_MS][TC_BN];         // column metadata ring (bulk-copied by the producer)
@@ -52,6 +56,24 @@ struct TcSmem {
     uint64_t mempty[TC_MS];
     uint32_t tmem_base;
 };
+constexpr int TC_SSTAGES = 2;            // streaming stages (96 KB each)
+template <>
+struct TcSmemT<true> {
+    uint8_t S[TC_SSTAGES][6][TC_PART];   // [stage][A blk0 hi, lo, A blk1 hi, lo, B hi, lo]
+    int32_t mcomp[TC_MS][TC_BN];
+    float mnorm[TC_MS][TC_BN];
+    float xa1[2 * TC_BM], xa2[2 * TC_BM];
+    int32_t xj1[2 * TC_BM];
+    uint64_t full[TC_STAGES];
+    uint64_t empty[TC_STAGES];
+    uint64_t afull;
+    uint64_t tfull[2];
+    uint64_t tempty[2];
+    uint64_t mfull[TC_MS];
+    uint64_t mempty[TC_MS];
+    uint32_t tmem_base;
+};
+using TcSmem = TcSmemT<false>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -132,13 +154,14 @@ __device__ __forceinline__ void tc_update(float a, int32_t j, float& a1, int32_t
     a1 = fminf(a1, a);
 }
 
+template <bool STREAM>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                  const int32_t* __restrict__ comp, int64_t n, int64_t row_lo, int64_t row_hi,
                  float kscale, float* __restrict__ out_a1, int32_t* __restrict__ out_j1,
-                 float* __restrict__ out_a2) {
+                 float* __restrict__ out_a2, int KA) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    TcSmem& sm = *reinterpret_cast<TcSmem*>(
+    TcSmemT<STREAM>& sm = *reinterpret_cast<TcSmemT<STREAM>*>(
         reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023)));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t blk0 = row_lo / TC_BM + 2 * (int64_t)blockIdx.x;   // first 128-row block
@@ -174,19 +197,39 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
     if (warp == 0) {
         // ------------------------------------------------ producer
         if (lane == 0) {
+          if constexpr (!STREAM) {
             mbar_expect_tx(&sm.afull, 4 * TC_PART);
             for (int r = 0; r < 2; ++r) {
                 const int64_t b = (blk0 + r < nblocks_total) ? blk0 + r : nblocks_total - 1;
                 bulk_g2s(sm.A[r][0], img + (b * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.afull);
                 bulk_g2s(sm.A[r][1], img + (b * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.afull);
             }
+          }
+            int64_t q = 0;   // stage uses (streaming)
             for (int64_t t = 0; t < ntiles; ++t) {
+              if constexpr (!STREAM) {
                 const int s = (int)(t % TC_STAGES);
                 const uint32_t ph = (uint32_t)((t / TC_STAGES) & 1);
                 if (t >= TC_STAGES) mbar_wait(&sm.empty[s], ph ^ 1);
                 mbar_expect_tx(&sm.full[s], 2 * TC_PART);
                 bulk_g2s(sm.B[s][0], img + (t * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
                 bulk_g2s(sm.B[s][1], img + (t * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+              } else {
+                // one stage per K atom: both row blocks' A atom and the tile's B atom
+                for (int a = 0; a < KA; ++a, ++q) {
+                    const int s = (int)(q % TC_SSTAGES);
+                    const uint32_t ph = (uint32_t)((q / TC_SSTAGES) & 1);
+                    if (q >= TC_SSTAGES) mbar_wait(&sm.empty[s], ph ^ 1);
+                    mbar_expect_tx(&sm.full[s], 6 * TC_PART);
+                    for (int r = 0; r < 2; ++r) {
+                        const int64_t b = (blk0 + r < nblocks_total) ? blk0 + r : nblocks_total - 1;
+                        bulk_g2s(sm.S[s][2 * r + 0], img + ((b * KA + a) * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+                        bulk_g2s(sm.S[s][2 * r + 1], img + ((b * KA + a) * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+                    }
+                    bulk_g2s(sm.S[s][4], img + ((t * KA + a) * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+                    bulk_g2s(sm.S[s][5], img + ((t * KA + a) * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+                }
+              }
                 // the tile's column components and norms for the epilogue
                 const int ms = (int)(t % TC_MS);
                 const uint32_t mph = (uint32_t)((t / TC_MS) & 1);
@@ -199,12 +242,14 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
-            mbar_wait(&sm.afull, 0);
+            if constexpr (!STREAM) mbar_wait(&sm.afull, 0);
+            int64_t q = 0;
             for (int64_t t = 0; t < ntiles; ++t) {
-                const int s = (int)(t % TC_STAGES);
-                const uint32_t ph = (uint32_t)((t / TC_STAGES) & 1);
                 const int as = (int)(t & 1);
                 if (t >= 2) mbar_wait(&sm.tempty[as], (uint32_t)(((t >> 1) - 1) & 1));
+              if constexpr (!STREAM) {
+                const int s = (int)(t % TC_STAGES);
+                const uint32_t ph = (uint32_t)((t / TC_STAGES) & 1);
                 mbar_wait(&sm.full[s], ph);
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll
@@ -220,6 +265,26 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                     }
                 }
                 umma_commit(&sm.empty[s]);
+              } else {
+                for (int a = 0; a < KA; ++a, ++q) {
+                    const int s = (int)(q % TC_SSTAGES);
+                    const uint32_t ph = (uint32_t)((q / TC_SSTAGES) & 1);
+                    mbar_wait(&sm.full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const uint32_t dcol = tmem + (uint32_t)(as * 256 + r * 128);
+#pragma unroll
+                        for (int step = 0; step < 12; ++step) {
+                            const int pass = step >> 2, kk = step & 3;
+                            const uint64_t da = umma_desc(sm.S[s][2 * r + (pass == 2 ? 1 : 0)]) + (uint64_t)(kk * 2);
+                            const uint64_t db = umma_desc(sm.S[s][4 + (pass == 1 ? 1 : 0)]) + (uint64_t)(kk * 2);
+                            umma_f16(dcol, da, db, (a > 0 || step > 0) ? 1u : 0u);
+                        }
+                    }
+                    umma_commit(&sm.empty[s]);
+                }
+              }
                 umma_commit(&sm.tfull[as]);
             }
         }
@@ -310,48 +375,59 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
 
 // Pre-swizzled FP16 split images: img[(block * 2 + part) * 16 KB], part 0 = hi,
 // 1 = lo; element (r, k) of a block at (r/8)*1024 + (r%8)*128 + ((k/8)^(r%8))*16 + (k%8)*2.
-__global__ void tc_image_kernel(const float* __restrict__ YT, int64_t npad, int d, float scale,
+__global__ void tc_image_kernel(const float* __restrict__ YT, int64_t npad, int d, int KA, float scale,
                                 int64_t nblocks, uint8_t* __restrict__ img) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one (point, k) pair
-    if (idx >= nblocks * TC_BM * 64) return;
-    const int k = (int)(idx & 63);
-    const int64_t p = idx >> 6;
+    if (idx >= nblocks * TC_BM * 64 * KA) return;
+    const int kg = (int)(idx % (64 * KA));
+    const int64_t p = idx / (64 * KA);
+    const int a = kg >> 6, k = kg & 63;
     const int64_t b = p / TC_BM;
     const int r = (int)(p % TC_BM);
-    const float y = (k < d && p < npad) ? YT[(int64_t)k * npad + p] * scale : 0.f;
+    const float y = (kg < d && p < npad) ? YT[(int64_t)kg * npad + p] * scale : 0.f;
     const __half hi = __float2half_rn(y);
     const __half lo = __float2half_rn(y - __half2float(hi));
     const int64_t off = (int64_t)(r >> 3) * 1024 + (r & 7) * 128 + (((k >> 3) ^ (r & 7)) << 4) + (k & 7) * 2;
-    *reinterpret_cast<__half*>(img + (b * 2 + 0) * (int64_t)TC_PART + off) = hi;
-    *reinterpret_cast<__half*>(img + (b * 2 + 1) * (int64_t)TC_PART + off) = lo;
+    *reinterpret_cast<__half*>(img + ((b * KA + a) * 2 + 0) * (int64_t)TC_PART + off) = hi;
+    *reinterpret_cast<__half*>(img + ((b * KA + a) * 2 + 1) * (int64_t)TC_PART + off) = lo;
 }
 
-size_t tc_image_bytes(int64_t n) {
+size_t tc_image_bytes(int64_t n, int d) {
     const int64_t nblocks = (n + TC_BM - 1) / TC_BM;
-    return (size_t)nblocks * 2 * TC_PART;
+    const int KA = (d + 63) / 64;
+    return (size_t)nblocks * KA * 2 * TC_PART;
 }
 
 cudaError_t launch_tc_image(const float* YT, int64_t npad, int d, float scale, int64_t n, uint8_t* img,
                             cudaStream_t st) {
     const int64_t nblocks = (n + TC_BM - 1) / TC_BM;
-    const int64_t total = nblocks * TC_BM * 64;
-    tc_image_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(YT, npad, d, scale, nblocks, img);
+    const int KA = (d + 63) / 64;
+    const int64_t total = nblocks * TC_BM * 64 * KA;
+    tc_image_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(YT, npad, d, KA, scale, nblocks, img);
     note_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_filter_tc(const uint8_t* img, const float* ny, const int32_t* comp, int64_t n,
+cudaError_t launch_filter_tc(const uint8_t* img, const float* ny, const int32_t* comp, int64_t n, int d,
                              int64_t lo, int64_t hi, float kscale, float* a1, int32_t* j1, float* a2,
                              cudaStream_t st) {
     if (hi <= lo) return cudaSuccess;
-    const size_t smem = sizeof(TcSmem) + 1024;
-    cudaError_t e = cudaFuncSetAttribute(filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
+    const int KA = (d + 63) / 64;
     const int64_t b_lo = lo / TC_BM, b_hi = (hi + TC_BM - 1) / TC_BM;
     const unsigned grid = (unsigned)((b_hi - b_lo + 1) / 2);
     const int pid = prof_begin(PK_FILTER, st);
-    filter_tc_kernel<<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, a1, j1, a2);
+    cudaError_t e;
+    if (KA == 1) {
+        const size_t smem = sizeof(TcSmemT<false>) + 1024;
+        e = cudaFuncSetAttribute(filter_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        filter_tc_kernel<false><<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, a1, j1, a2, 1);
+    } else {
+        const size_t smem = sizeof(TcSmemT<true>) + 1024;
+        e = cudaFuncSetAttribute(filter_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        filter_tc_kernel<true><<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, a1, j1, a2, KA);
+    }
     prof_end(pid, st);
     note_launch();
     return cudaGetLastError();

@@ -72,10 +72,10 @@ cudaError_t launch_hook_contract(int32_t* comp, int64_t n, const unsigned long l
                                  int32_t* changed, int32_t* nroots, cudaStream_t st);
 
 // filter_tc.cu
-size_t tc_image_bytes(int64_t n);
+size_t tc_image_bytes(int64_t n, int d);
 cudaError_t launch_tc_image(const float* YT, int64_t npad, int d, float scale, int64_t n, uint8_t* img,
                             cudaStream_t st);
-cudaError_t launch_filter_tc(const uint8_t* img, const float* ny, const int32_t* comp, int64_t n,
+cudaError_t launch_filter_tc(const uint8_t* img, const float* ny, const int32_t* comp, int64_t n, int d,
                              int64_t lo, int64_t hi, float kscale, float* a1, int32_t* j1, float* a2,
                              cudaStream_t st);
 cudaError_t launch_absmax(const float* v, int64_t m, uint32_t* out, cudaStream_t st);
