@@ -79,6 +79,19 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// explicit shared-memory vector loads (the dynamic-smem struct is reached
+// through an aligned generic pointer, which would otherwise become LD.E)
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int4 lds_i4(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -321,8 +334,8 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                 float m = INFINITY;
 #pragma unroll
                 for (int i4 = 0; i4 < 8; ++i4) {
-                    const float4 cn4 = *reinterpret_cast<const float4*>(&sm.mnorm[ms][lc0 + 4 * i4]);
-                    const int4 cc4 = *reinterpret_cast<const int4*>(&sm.mcomp[ms][lc0 + 4 * i4]);
+                    const float4 cn4 = lds_f4(smem_u32(&sm.mnorm[ms][lc0 + 4 * i4]));
+                    const int4 cc4 = lds_i4(smem_u32(&sm.mcomp[ms][lc0 + 4 * i4]));
                     const float cn[4] = {cn4.x, cn4.y, cn4.z, cn4.w};
                     const int32_t cc[4] = {cc4.x, cc4.y, cc4.z, cc4.w};
 #pragma unroll
