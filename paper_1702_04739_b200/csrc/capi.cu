@@ -428,10 +428,7 @@ int isoc_omega(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi, do
     if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
     if (!(sigma > 0.0)) return fail(ISOC_EINVAL, "sigma must be > 0, got %g", sigma);
     if (lo < 0 || hi > n || lo >= hi) return fail(ISOC_EINVAL, "bad row range");
-    ensure_pool();
-    CK(launch_omega_pass(X, n, d, lo, hi, sigma, nullptr, omega, nullptr, nullptr, nullptr,
-                         (cudaStream_t)stream));
-    return ISOC_OK;
+    return isoc_omega_mst(X, n, d, lo, hi, sigma, nullptr, omega, nullptr, nullptr, nullptr, stream);
 }
 
 int isoc_omega_mst(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi, double sigma,
@@ -443,7 +440,14 @@ int isoc_omega_mst(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi
     ensure_pool();
     const int32_t* comp = h ? h->comp : nullptr;
     if (h && (h->lo != lo || h->hi != hi)) return fail(ISOC_EINVAL, "MST handle rows differ");
-    if (lo == 0 && hi == n) {
+    // the symmetric pass keeps one 1024-wide subtree (+ round-2 minimum) per
+    // (block, row): 20 B x n^2 / 1024 -- use it while that fits comfortably
+    const int64_t nbs = (n + 1023) / 1024;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const double ps_bytes = (double)nbs * (double)n * (comp ? 20.0 : 8.0);
+    const bool sym_fits = ps_bytes < 0.6 * (double)free_b;
+    if (lo == 0 && hi == n && sym_fits && getenv("ISOC_OMEGA_ROWS") == nullptr) {
         CK(launch_omega_sym(X, n, d, sigma, comp, omega, nn_j, nn_d, nn_tie, (cudaStream_t)stream));
     } else {
         CK(launch_omega_pass(X, n, d, lo, hi, sigma, comp, omega, nn_j, nn_d, nn_tie,
