@@ -107,6 +107,14 @@ class CudaBackend:
     def empty(self, shape, dtype):
         return self.torch.empty(shape, dtype=dtype, device=self.device)
 
+    _NP2TORCH = {np.dtype(np.int64): "int64", np.dtype(np.float64): "float64", np.dtype(np.int8): "int8",
+                 np.dtype(np.int32): "int32"}
+
+    def pinned_empty(self, n: int, dtype) -> np.ndarray:
+        """numpy view of a page-locked host buffer (the array keeps it alive)."""
+        tdt = getattr(self.torch, self._NP2TORCH[np.dtype(dtype)])
+        return self.torch.empty(n, dtype=tdt, pin_memory=True).numpy()
+
     # -- exact passes -------------------------------------------------
     def sigma_partial(self, X, n: int, d: int, lo: int, hi: int, alpha: float, want_nn: bool = True):
         torch = self.torch
@@ -231,14 +239,18 @@ class DeviceTree:
             except Exception:
                 pass
 
+    def _host(self, n: int, dtype):
+        """Page-locked host array (device->host copies at full PCIe/C2C rate)."""
+        return self.b.pinned_empty(n, dtype)
+
     def export(self):
         n = self.n
-        parent = np.empty(n, np.int64)
-        flow = np.empty(n, np.float64)
-        depth = np.empty(n, np.int64)
-        cid = np.empty(n, np.int64)
-        order = np.empty(n, np.int64)
-        pdist = np.empty(n, np.float64)
+        parent = self._host(n, np.int64)
+        flow = self._host(n, np.float64)
+        depth = self._host(n, np.int64)
+        cid = self._host(n, np.int64)
+        order = self._host(n, np.int64)
+        pdist = self._host(n, np.float64)
         md = ctypes.c_int64()
         check(self.b.lib.isoc_tree_export(self.h, parent.ctypes.data, flow.ctypes.data, depth.ctypes.data,
                                           cid.ctypes.data, order.ctypes.data, ctypes.byref(md),
@@ -270,9 +282,9 @@ class DeviceTree:
 
     def witness(self, slot: int, k: int) -> Witness:
         n = self.n
-        labels = np.empty(n, np.int64)
-        cut = np.empty(n, np.int8)
-        eta = np.empty(n, np.int64)
+        labels = self._host(n, np.int64)
+        cut = self._host(n, np.int8)
+        eta = self._host(n, np.int64)
         sp = np.empty(k, np.float64)
         miso = ctypes.c_double()
         check(self.b.lib.isoc_witness(self.h, int(slot), int(k), labels.ctypes.data, cut.ctypes.data,

@@ -31,6 +31,7 @@ import numpy as np
 from ._lib import InfeasibleSubpartitionError
 from .engine import Comm, CudaBackend, DeviceTree
 from .types import (
+    LazyRootedTree,
     BRACKET_EPS,
     MAX_ITERATIONS,
     NO_VERTEX,
@@ -222,8 +223,7 @@ def _progress(c: int, comps: int, stats: dict) -> int:
 
 
 def _rooted_tree_view(dt: DeviceTree, root: int) -> RootedTree:
-    parent, flow, depth, cid, order, max_depth, _ = dt.export()
-    return RootedTree(parent, flow, depth, cid, order, int(root), max_depth, _device=dt)
+    return LazyRootedTree(dt, root)
 
 
 def auto_sigma(points) -> float:
@@ -275,19 +275,21 @@ def total_distance(tree: RootedTree) -> float:
 
 def tree_from_parent_list(parent, parent_flow, root: Optional[int] = None) -> RootedTree:
     """mst.py:78-125 on the device (sibling ranks by ascending vertex index)."""
-    par = np.asarray(parent, dtype=np.int64).copy()
-    flows = np.asarray(parent_flow, dtype=np.float64).copy()
+    # inputs are read, never mutated (the device keeps its own copies)
+    par = np.ascontiguousarray(parent, dtype=np.int64)
+    flows = np.ascontiguousarray(parent_flow, dtype=np.float64)
     n = par.shape[0]
     if par.ndim != 1 or flows.shape != par.shape:
         raise ValueError("parent and parent_flow must be 1-d arrays of equal length")
-    roots = np.flatnonzero(par == NO_VERTEX)
+    is_root = par == NO_VERTEX
+    nroots = int(np.count_nonzero(is_root))
     if root is None:
-        if roots.size != 1:
-            raise ValueError(f"expected exactly one root sentinel, found {roots.size}")
-        root = int(roots[0])
-    elif roots.size != 1 or int(roots[0]) != root:
+        if nroots != 1:
+            raise ValueError(f"expected exactly one root sentinel, found {nroots}")
+        root = int(np.argmax(is_root))
+    elif nroots != 1 or not (0 <= root < n) or not bool(is_root[root]):
         raise ValueError("root does not match the parent array's sentinel")
-    if (par[np.arange(n) != root] < 0).any() or (par >= n).any():
+    if n and (int(par.min()) < NO_VERTEX or int(par.max()) >= n):
         raise ValueError("parent indices out of range")
     dt = backend().tree_from_parent(par, flows, root)
     return _rooted_tree_view(dt, root)

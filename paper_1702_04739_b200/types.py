@@ -78,6 +78,31 @@ class RootedTree:
         return self.parent.shape[0]
 
 
+class LazyRootedTree(RootedTree):
+    """RootedTree whose arrays stay on the device until first read (one
+    export of all five arrays); solve_miso / extrema use the device tree
+    directly, so a caller that only wants the partition never pays the
+    device-to-host copy of the tree."""
+
+    _LAZY = ("parent", "parent_flow", "depth", "child_id", "bfs_order", "max_depth")
+
+    def __init__(self, device_tree, root: int):
+        object.__setattr__(self, "_device", device_tree)
+        object.__setattr__(self, "root", int(root))
+
+    def __getattr__(self, name):
+        if name in LazyRootedTree._LAZY:
+            parent, flow, depth, cid, order, max_depth, _ = self._device.export()
+            for k, v in zip(LazyRootedTree._LAZY, (parent, flow, depth, cid, order, max_depth)):
+                object.__setattr__(self, k, v)
+            return object.__getattribute__(self, name)
+        raise AttributeError(name)
+
+    @property
+    def n(self) -> int:
+        return self._device.n
+
+
 @dataclass(eq=False)
 class DecisionOutcome:
     """Result of one threshold decision sweep (isoperim.py:37-50)."""
