@@ -395,13 +395,14 @@ rescan_tile_kernel(const double* __restrict__ X, int64_t n, int d, const int32_t
                    const int32_t* __restrict__ rescan_list, const int32_t* __restrict__ rescan_count,
                    int64_t nchunks, double* __restrict__ pm1, double* __restrict__ pm2,
                    int32_t* __restrict__ pj) {
-    __shared__ double As[RKC][RR];
-    __shared__ double Bs[RKC][129];
+    __shared__ double As[2][RKC][RR];
+    __shared__ double Bs[2][RKC][129];
     __shared__ int32_t crow[RR];
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const int64_t cnt = *rescan_count;
     const int64_t ngroups = (cnt + RR - 1) / RR;
     const int64_t items = ngroups * nchunks;
+    const int nkc = (d + RKC - 1) / RKC;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
         const int64_t g = item / nchunks, c = item % nchunks;
         __syncthreads();
@@ -420,35 +421,57 @@ rescan_tile_kernel(const double* __restrict__ X, int64_t n, int d, const int32_t
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-            for (int k0 = 0; k0 < d; k0 += RKC) {
-                __syncthreads();
+            // k chunks through registers into a double-buffered tile: the
+            // global loads of chunk kc+1 are in flight while chunk kc computes
+            double ra[2], rb[8];
+            auto gload = [&](int k0) {
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int idx = tid + 256 * e;
                     const int r = idx / RKC, kk = idx % RKC;
                     const int64_t q = g * RR + r;
-                    As[kk][r] = (q < cnt && k0 + kk < d) ? X[(int64_t)rescan_list[q] * d + k0 + kk] : 0.0;
+                    ra[e] = (q < cnt && k0 + kk < d) ? X[(int64_t)rescan_list[q] * d + k0 + kk] : 0.0;
                 }
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const int idx = tid + 256 * e;
                     const int j = idx / RKC, kk = idx % RKC;
                     const int64_t col = t0 + j;
-                    Bs[kk][j] = (col < n && k0 + kk < d) ? X[col * d + k0 + kk] : 0.0;
+                    rb[e] = (col < n && k0 + kk < d) ? X[col * d + k0 + kk] : 0.0;
                 }
-                __syncthreads();
+            };
+            auto sstore = [&](int buf) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int idx = tid + 256 * e;
+                    As[buf][idx % RKC][idx / RKC] = ra[e];
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int idx = tid + 256 * e;
+                    Bs[buf][idx % RKC][idx / RKC] = rb[e];
+                }
+            };
+            gload(0);
+            sstore(0);
+            __syncthreads();
+            for (int kc = 0; kc < nkc; ++kc) {
+                if (kc + 1 < nkc) gload((kc + 1) * RKC);
+                const int buf = kc & 1;
 #pragma unroll
                 for (int kk = 0; kk < RKC; ++kk) {
                     double a[4], bb[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 8 * i];
+                    for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][ty + 8 * i];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tx + 32 * j];
+                    for (int j = 0; j < 4; ++j) bb[j] = Bs[buf][kk][tx + 32 * j];
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
 #pragma unroll
                         for (int j = 0; j < 4; ++j) acc[i][j] = exact_sq_step(acc[i][j], a[i], bb[j]);
                 }
+                if (kc + 1 < nkc) sstore((kc + 1) & 1);
+                __syncthreads();
             }
             // zero-padded k beyond d adds exact zeros: (0-0)^2 = 0
 #pragma unroll
