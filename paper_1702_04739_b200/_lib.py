@@ -18,6 +18,7 @@ CSRC = os.path.join(_HERE, "csrc")
 
 ISOC_OK, ISOC_EINVAL, ISOC_ETYPE, ISOC_EINFEASIBLE, ISOC_ENOMEM, ISOC_ECUDA = range(6)
 FOLD_STACK_BYTES = 1544
+ROW_CAP = 40          # per-row leaf-stack entries of the sigma passes (csrc/kernels.h kRowCap)
 
 _lock = threading.Lock()
 _lib = None
@@ -59,6 +60,9 @@ SIGNATURES = {
     "isoc_last_error": (ctypes.c_char_p, []),
     "isoc_sigma_partial": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P, P, P, P, P]),
     "isoc_sigma_finish": (ctypes.c_int, [P, I64, PD, P]),
+    "isoc_sym_block_range": (ctypes.c_int, [I64, I32, I32, PI64, PI64]),
+    "isoc_sigma_sym_range": (ctypes.c_int, [P, I64, I32, I64, I64, P, P, P, P, P, P, P]),
+    "isoc_sigma_rank_merge": (ctypes.c_int, [P, I64, I32, I64, I64, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "isoc_omega": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P]),
     "isoc_omega_mst": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P, P, P, P, P]),
     "isoc_mst_create": (ctypes.c_int, [P, I64, I32, I64, I64, P, ctypes.POINTER(P)]),

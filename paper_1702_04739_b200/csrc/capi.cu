@@ -217,6 +217,74 @@ int isoc_sigma_partial(const double* X, int64_t n, int32_t d, int64_t lo, int64_
     return ISOC_OK;
 }
 
+int isoc_sym_block_range(int64_t n, int32_t rank, int32_t world, int64_t* jlo, int64_t* jhi) {
+    if (n < 1 || world < 1 || rank < 0 || rank >= world) return fail(ISOC_EINVAL, "bad rank/world");
+    sym_block_range(n, rank, world, jlo, jhi);
+    return ISOC_OK;
+}
+
+int isoc_sigma_sym_range(const double* X, int64_t n, int32_t d, int64_t jlo, int64_t jhi, double* vals,
+                         uint64_t* ids, int32_t* cnt, double* m1, double* m2, int32_t* j1, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
+    if (n > (int64_t)INT32_MAX) return fail(ISOC_EINVAL, "n too large");
+    const int64_t nbs = (n + 1023) / 1024;
+    if (jlo < 0 || jhi > nbs || jlo > jhi) return fail(ISOC_EINVAL, "bad block range [%lld, %lld)", (long long)jlo, (long long)jhi);
+    ensure_pool();
+    int32_t* flags = nullptr;
+    CK(aalloc(&flags, 1, st));
+    CK(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    CK(launch_sigma_sym_range(X, n, d, jlo, jhi, 1, vals, ids, cnt, flags, m1 ? j1 : nullptr, m1, nullptr, m2, st));
+    int32_t hflags = 0;
+    CK(cudaMemcpyAsync(&hflags, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(flags, st);
+    CK(cudaStreamSynchronize(st));
+    if (hflags) return fail(ISOC_ECUDA, "pairwise fold stack overflow (flags=%d)", hflags);
+    return ISOC_OK;
+}
+
+int isoc_sigma_rank_merge(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi, int32_t G,
+                          const double* vals, const uint64_t* ids, const int32_t* cnt, const double* m1,
+                          const double* m2, const int32_t* j1, void* stack_dev, int32_t* nn_j, double* nn_d,
+                          int8_t* nn_tie, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
+    if (lo < 0 || hi > n || lo >= hi) return fail(ISOC_EINVAL, "bad row range");
+    if (G < 1) return fail(ISOC_EINVAL, "need at least one rank");
+    ensure_pool();
+    const int64_t rows = hi - lo;
+    double* row_vals = nullptr;
+    int32_t *row_cnt = nullptr, *flags = nullptr;
+    uint64_t *row_ids = nullptr, *sid = nullptr;
+    double* sval = nullptr;
+    int8_t* sown = nullptr;
+    FoldStack* groups = nullptr;
+    CK(aalloc(&row_vals, sigma_rowstack_entries(rows), st));
+    CK(aalloc(&row_ids, sigma_rowstack_entries(rows), st));
+    CK(aalloc(&row_cnt, rows, st));
+    CK(aalloc(&flags, 1, st));
+    CK(aalloc(&sval, rows, st));
+    CK(aalloc(&sid, rows, st));
+    CK(aalloc(&sown, rows, st));
+    const int64_t ng = (rows + 63) / 64;
+    CK(aalloc(&groups, ng, st));
+    CK(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    CK(cudaMemsetAsync(sown, 0, rows, st));
+    CK(launch_sigma_rank_merge(rows, G, vals, ids, cnt, m1, m2, j1, row_vals, row_ids, row_cnt, flags,
+                               (m1 && nn_j) ? nn_j : nullptr, nn_d, nn_tie, st));
+    CK(launch_sigma_straddle(X, n, d, lo + 1, hi + 1, sval, sid, sown, st));
+    CK(launch_sigma_merge_rows(n, lo, hi, 64, row_vals, row_ids, row_cnt, sval, sid, sown, groups, flags, st));
+    CK(fold_stacks(groups, ng, reinterpret_cast<FoldStack*>(stack_dev), flags, st));
+    int32_t hflags = 0;
+    CK(cudaMemcpyAsync(&hflags, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(row_vals, st); cudaFreeAsync(row_ids, st); cudaFreeAsync(row_cnt, st);
+    cudaFreeAsync(sval, st); cudaFreeAsync(sid, st); cudaFreeAsync(sown, st);
+    cudaFreeAsync(groups, st); cudaFreeAsync(flags, st);
+    CK(cudaStreamSynchronize(st));
+    if (hflags) return fail(ISOC_ECUDA, "pairwise fold stack overflow (flags=%d)", hflags);
+    return ISOC_OK;
+}
+
 int isoc_sigma_finish(const void* stacks_dev, int64_t nseg, double* total_host, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (nseg < 1) return fail(ISOC_EINVAL, "no fold stacks");

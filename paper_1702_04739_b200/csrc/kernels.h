@@ -34,6 +34,15 @@ bool sigma_sym_applicable(int64_t n, int64_t lo, int64_t hi, int want_p);
 cudaError_t launch_sigma_sym(const double* X, int64_t n, int d, double* row_vals, uint64_t* row_ids,
                              int32_t* row_cnt, int32_t* flags, int32_t* nn_j, double* nn_d,
                              int8_t* nn_tie, cudaStream_t st);
+cudaError_t launch_sigma_sym_range(const double* X, int64_t n, int d, int64_t jlo, int64_t jhi, int partial,
+                                   double* row_vals, uint64_t* row_ids, int32_t* row_cnt, int32_t* flags,
+                                   int32_t* nn_j, double* nn_d, int8_t* nn_tie, double* nn_m2,
+                                   cudaStream_t st);
+cudaError_t launch_sigma_rank_merge(int64_t rows, int G, const double* pv, const uint64_t* pid_,
+                                    const int32_t* pc, const double* pm1, const double* pm2, const int32_t* pj,
+                                    double* row_vals, uint64_t* row_ids, int32_t* row_cnt, int32_t* flags,
+                                    int32_t* nn_j, double* nn_d, int8_t* nn_tie, cudaStream_t st);
+void sym_block_range(int64_t n, int rank, int world, int64_t* jlo, int64_t* jhi);
 
 // omega_sym.cu
 cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, const int32_t* comp,

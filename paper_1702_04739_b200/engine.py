@@ -68,6 +68,23 @@ class Comm:
         self.dist.all_gather(parts, pad)
         return torch.cat([p[: h - l] for p, (l, h) in zip(parts, sizes)])
 
+    def alltoall_rows(self, t, n: int):
+        """Rows of `t` (n rows, any trailing shape) sent to their owners; the
+        result holds, rank-major, every rank's rows of this rank's shard:
+        shape (world, hi - lo, ...).  Ranks exchange equal padded blocks."""
+        torch = _torch()
+        lo, hi = self.rows(n)
+        if self.world == 1:
+            return t[lo:hi].unsqueeze(0)
+        sizes = [self.rows(n, r) for r in range(self.world)]
+        mx = max(h - l for l, h in sizes)
+        send = torch.zeros((self.world, mx) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        for r, (l, h) in enumerate(sizes):
+            send[r, : h - l] = t[l:h]
+        recv = torch.empty_like(send)
+        self.dist.all_to_all_single(recv, send)
+        return recv[:, : hi - lo].contiguous()
+
     def allgather_stack(self, stack):
         """Fold stacks of every rank, in rank (= row) order."""
         if self.world == 1:
@@ -137,6 +154,49 @@ class CudaBackend:
         check(self.lib.isoc_sigma_finish(_ptr(stacks), stacks.shape[0], ctypes.byref(total),
                                          self.stream))
         return total.value
+
+    def sym_block_range(self, n: int, rank: int, world: int) -> tuple:
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        check(self.lib.isoc_sym_block_range(n, rank, world, ctypes.byref(lo), ctypes.byref(hi)))
+        return int(lo.value), int(hi.value)
+
+    def sigma_sym_range(self, X, n: int, d: int, jlo: int, jhi: int, want_nn: bool = True):
+        """This rank's partial leaf stacks and neighbours for all n rows."""
+        torch = self.torch
+        vals = self.empty((n, _lib.ROW_CAP), torch.float64)
+        ids = self.empty((n, _lib.ROW_CAP), torch.int64)
+        cnt = self.empty((n,), torch.int32)
+        if want_nn:
+            m1, m2, j1 = (self.empty((n,), torch.float64), self.empty((n,), torch.float64),
+                          self.empty((n,), torch.int32))
+            nnp = (_ptr(m1), _ptr(m2), _ptr(j1))
+        else:
+            m1 = m2 = j1 = None
+            nnp = (None, None, None)
+        check(self.lib.isoc_sigma_sym_range(_ptr(X), n, d, jlo, jhi, _ptr(vals), _ptr(ids), _ptr(cnt), *nnp,
+                                            self.stream))
+        return vals, ids, cnt, m1, m2, j1
+
+    def sigma_rank_merge(self, X, n: int, d: int, lo: int, hi: int, parts, want_nn: bool = True):
+        """Owner side: parts = (vals, ids, cnt, m1, m2, j1) rank-major for
+        rows [lo, hi); returns (fold stack, nn) like sigma_partial."""
+        torch = self.torch
+        vals, ids, cnt, m1, m2, j1 = parts
+        G = vals.shape[0]
+        rows = hi - lo
+        stack = self.empty((_lib.FOLD_STACK_BYTES,), torch.uint8)
+        if want_nn and m1 is not None:
+            nn_j = self.empty((rows,), torch.int32)
+            nn_d = self.empty((rows,), torch.float64)
+            nn_tie = self.empty((rows,), torch.int8)
+            nnin = (_ptr(m1), _ptr(m2), _ptr(j1))
+            nnout = (_ptr(nn_j), _ptr(nn_d), _ptr(nn_tie))
+        else:
+            nnin = (None, None, None)
+            nnout = (None, None, None)
+        check(self.lib.isoc_sigma_rank_merge(_ptr(X), n, d, lo, hi, G, _ptr(vals), _ptr(ids), _ptr(cnt), *nnin,
+                                             _ptr(stack), *nnout, self.stream))
+        return stack, ((nn_j, nn_d, nn_tie) if (want_nn and m1 is not None) else None)
 
     def omega(self, X, n: int, d: int, lo: int, hi: int, sigma: float):
         out = self.empty((hi - lo,), self.torch.float64)

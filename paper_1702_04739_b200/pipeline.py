@@ -134,7 +134,22 @@ class _Points:
         self.lo, self.hi = self.comm.rows(self.n)
 
 
+def _sharded_symmetric(P: _Points, alpha: float = 0.0) -> bool:
+    """Multi-GPU: the symmetric passes sharded by column-super-block ranges
+    (each unordered pair once across the job) instead of row shards of the
+    one-sided passes.  ISOC_SHARDED_SYM=0 selects the row shards."""
+    return (P.comm.world > 1 and alpha == 0.0 and P.n >= 2048 and hasattr(P.b, "sigma_sym_range")
+            and os.environ.get("ISOC_SHARDED_SYM", "1") != "0")
+
+
 def _sigma_pass(P: _Points, alpha: float, want_nn: bool = True):
+    if _sharded_symmetric(P, alpha):
+        jlo, jhi = P.b.sym_block_range(P.n, P.comm.rank, P.comm.world)
+        part = P.b.sigma_sym_range(P.X, P.n, P.d, jlo, jhi, want_nn)
+        recv = tuple(None if t is None else P.comm.alltoall_rows(t, P.n) for t in part)
+        stack, nn = P.b.sigma_rank_merge(P.X, P.n, P.d, P.lo, P.hi, recv, want_nn)
+        p_loc = P.b.empty((P.hi - P.lo,), P.b.torch.float64).zero_()
+        return stack, nn, p_loc
     if want_nn:
         return P.b.sigma_partial(P.X, P.n, P.d, P.lo, P.hi, alpha)
     return P.b.sigma_partial(P.X, P.n, P.d, P.lo, P.hi, alpha, want_nn=False)
