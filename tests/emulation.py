@@ -141,6 +141,105 @@ class EmuBackend:
         nn = (torch.from_numpy(nn_j), torch.from_numpy(nn_d), torch.from_numpy(nn_tie)) if want_nn else None
         return pack_stack(st), nn, torch.from_numpy(p)
 
+    # sharded symmetric sigma (pipeline._sigma_pass with world > 1): the
+    # rank's per-row partial stacks over its column-block range, restated
+    SYM_BLOCK = 1024
+
+    def sym_block_range(self, n, rank, world):
+        import math
+        nbs = -(-n // self.SYM_BLOCK)
+        tot = nbs * (nbs + 1) / 2.0
+
+        def bound(k):
+            if k <= 0:
+                return 0
+            if k >= world:
+                return nbs
+            target = tot * k / world
+            return max(0, min(nbs, int(math.ceil((math.sqrt(8.0 * target + 1.0) - 1.0) / 2.0))))
+        return bound(rank), bound(rank + 1)
+
+    def sigma_sym_range(self, X, n, d, jlo, jhi, want_nn=True):
+        Xn = X.numpy()
+        total, B = n * n, self.SYM_BLOCK
+        cap = 40
+        vals = np.zeros((n, cap))
+        ids = np.zeros((n, cap), np.int64)
+        cnt = np.zeros(n, np.int32)
+        m1 = np.full(n, np.inf)
+        m2 = np.full(n, np.inf)
+        j1 = np.full(n, 2**31 - 1, np.int32)
+        rows = orc.distance_rows(Xn, 0, n)
+        for r in range(n):
+            K = r // B
+            if K < jlo:
+                a, b = jlo, jhi
+            elif K < jhi:
+                a, b = 0, jhi
+            else:
+                continue
+            rs, re = r * n, (r + 1) * n
+            # internal leaves of the row (as sigma_partial) starting in [a*B, b*B)
+            st = []
+            s_, l, h = find_leaf(total, rs)
+            if s_ < rs:
+                s_, l, h = find_leaf(total, s_ + l) if s_ + l < re else (re, 0, 0)
+            while l > 0 and s_ + l <= re and not (s_ + l == total and total % 8):
+                if rs + a * B <= s_ < rs + b * B:
+                    push(st, leaf_sum(rows[r][s_ - rs:s_ + l - rs]), h)
+                if s_ + l >= re:
+                    break
+                s_, l, h = find_leaf(total, s_ + l)
+            cnt[r] = len(st)
+            for e, (v, hh) in enumerate(st):
+                vals[r, e], ids[r, e] = v, np.uint64(hh).view(np.int64)
+            if want_nn:
+                row = rows[r][a * B:min(b * B, n)].copy()
+                if a * B <= r < b * B:
+                    row[r - a * B] = np.inf
+                if row.size and np.isfinite(row.min()):
+                    j = int(np.argmin(row))
+                    m1[r], j1[r] = row[j], a * B + j
+                    rr = row.copy()
+                    rr[j] = np.inf
+                    m2[r] = rr.min()
+        t = torch.from_numpy
+        nnp = (t(m1), t(m2), t(j1)) if want_nn else (None, None, None)
+        return (t(vals), t(ids), t(cnt)) + nnp
+
+    def sigma_rank_merge(self, X, n, d, lo, hi, parts, want_nn=True):
+        Xn = X.numpy()
+        total = n * n
+        vals, ids, cnt, m1, m2, j1 = parts
+        G = vals.shape[0]
+        st = []
+        nn_j = np.zeros(hi - lo, np.int32)
+        nn_d = np.zeros(hi - lo)
+        nn_tie = np.zeros(hi - lo, np.int8)
+        for i in range(lo, hi):
+            q = i - lo
+            if i > lo:
+                self._straddle(Xn, n, total, i, st)
+            for g in range(G):
+                for e in range(int(cnt[g, q])):
+                    push(st, float(vals[g, q, e]), int(np.int64(ids[g, q, e]).view(np.uint64)))
+            if want_nn and m1 is not None:
+                best = (np.inf, 2**31 - 1)
+                sec = np.inf
+                for g in range(G):
+                    c = (float(m1[g, q]), int(j1[g, q]))
+                    if c < best:
+                        sec = min(sec, best[0], float(m2[g, q]))
+                        best = c
+                    else:
+                        sec = min(sec, c[0])
+                nn_j[q] = -1 if best[1] == 2**31 - 1 else best[1]
+                nn_d[q] = best[0]
+                nn_tie[q] = int(sec == best[0])
+        self._straddle(Xn, n, total, hi, st)
+        nn = (torch.from_numpy(nn_j), torch.from_numpy(nn_d), torch.from_numpy(nn_tie)) if want_nn else None
+        return pack_stack(st), nn
+
     @staticmethod
     def _straddle(Xn, n, total, b, st):
         if b < n:

@@ -77,3 +77,55 @@ def test_sharded_host_logic_matches_single_rank_and_oracle(n, d, k, oracle_mod):
         assert [(a, b) for a, b, _ in r["edges"]] == prim_edges, w
         assert np.array_equal(r["omega"].view(np.int64), omega.view(np.int64)), w
         assert r["edges"] == res[1]["edges"]
+
+
+def _sigma_worker(rank, world, port, n, d, k, out_path):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    for p in (os.path.dirname(here), here, os.path.join(os.path.dirname(here), "oracle")):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle as orc
+    from emulation import EmuBackend
+    from paper_1702_04739_b200 import pipeline as pl
+    from paper_1702_04739_b200.engine import Comm
+
+    X, _ = orc.generate_random(n, d, k, 5)
+    X[7] = X[n - 3]                      # an exact duplicate: a neighbour tie
+    comm = Comm()
+    P = pl._Points(X, comm=comm, b=EmuBackend())
+    assert pl._sharded_symmetric(P) == (world > 1)
+    stack, nn, _ = pl._sigma_pass(P, 0.0)
+    sigma = pl._sigma_from_stack(P, stack)
+    nn_all = [comm.allgather_rows(t, n).numpy() for t in nn]
+    if rank == 0:
+        with open(out_path, "wb") as fh:
+            pickle.dump({"sigma": sigma, "nn": nn_all}, fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_symmetric_sigma_host_logic(world, oracle_mod):
+    """Column-block ranges per rank, the all-to-all of per-row partial stacks
+    and the rank-order merge (gloo, CPU emulation of the kernels) give the
+    oracle's sigma and the row pass's nearest neighbours and tie flags."""
+    n, d, k = 2100, 3, 4
+    X, _ = oracle_mod.generate_random(n, d, k, 5)
+    X[7] = X[n - 3]
+    with tempfile.TemporaryDirectory() as tmp:
+        out = os.path.join(tmp, "s.pkl")
+        mp.spawn(_sigma_worker, args=(world, _free_port(), n, d, k, out), nprocs=world, join=True)
+        with open(out, "rb") as fh:
+            r = pickle.load(fh)
+    assert r["sigma"] == oracle_mod.auto_sigma(X)
+    rows = oracle_mod.distance_rows(X, 0, n)
+    np.fill_diagonal(rows, np.inf)
+    j = rows.argmin(axis=1)
+    assert np.array_equal(r["nn"][0], j)
+    assert np.array_equal(r["nn"][1], rows[np.arange(n), j])
+    srt = np.sort(rows, axis=1)
+    assert np.array_equal(r["nn"][2], (srt[:, 0] == srt[:, 1]).astype(np.int8))
