@@ -81,6 +81,19 @@ __device__ __forceinline__ void sym_load(SymStage& s, const double* __restrict__
     }
 }
 
+// Slot of the 1024-wide subtree of row i over super-block b.  One GPU:
+// [b][i] (G = 1, rows_pad = n).  Sharded (G ranks, rank r owning rows
+// [n*r/G, n*(r+1)/G)): [owner(i)][b][i - lo(owner)], so each owner's slots
+// are one contiguous chunk of an all-to-all.
+__host__ __device__ __forceinline__ int64_t ps_slot(int64_t b, int64_t i, int64_t n, int64_t nbs, int G,
+                                                    int64_t rows_pad) {
+    if (G == 1) return b * n + i;
+    int64_t r = i * G / n;
+    while (n * (r + 1) / G <= i) ++r;
+    while (n * r / G > i) --r;
+    return (r * nbs + b) * rows_pad + (i - n * r / G);
+}
+
 __device__ __forceinline__ bool lex_less(double a, int32_t ja, double b, int32_t jb) {
     return a < b || (a == b && ja < jb);
 }
@@ -113,7 +126,7 @@ __device__ __forceinline__ void token_pass(int team) {
 __global__ void __launch_bounds__(STH, 1)
 omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n, int64_t nbs,
                  double sigma, double rs, const int32_t* __restrict__ comp, double* __restrict__ PS,
-                 double* __restrict__ PSm, int32_t* __restrict__ PSj) {
+                 double* __restrict__ PSm, int32_t* __restrict__ PSj, int64_t b0, int G, int64_t rows_pad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SymSmem& sm = *reinterpret_cast<SymSmem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -125,7 +138,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
     // lanes of a row group read 8 consecutive 16-byte chunks (no bank
     // conflicts); thread rows: 4*rg + i, i < 4
     // triangular decode of blockIdx -> (I, J), I <= J
-    const int64_t b = blockIdx.x;
+    const int64_t b = b0 + blockIdx.x;
     int64_t J = (int64_t)((sqrt(8.0 * (double)b + 1.0) - 1.0) / 2.0);
     while ((J + 1) * (J + 2) / 2 <= b) ++J;
     while (J * (J + 1) / 2 > b) --J;
@@ -293,13 +306,14 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                     } else {
                         const int64_t gi = R0 + ti * TBM + r;
                         if (gi < n) {
-                            PS[J * n + gi] = __dadd_rn(sm.rowv[r], half);
+                            const int64_t o = ps_slot(J, gi, n, nbs, G, rows_pad);
+                            PS[o] = __dadd_rn(sm.rowv[r], half);
                             if (want_min) {
                                 double m = sm.rowm[r];
                                 int32_t mj = sm.rowj[r];
                                 if (lex_less(ts.rmin[r], ts.rminj[r], m, mj)) { m = ts.rmin[r]; mj = ts.rminj[r]; }
-                                PSm[J * n + gi] = m;
-                                PSj[J * n + gi] = mj;
+                                PSm[o] = m;
+                                PSj[o] = mj;
                             }
                         }
                     }
@@ -345,26 +359,31 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
         for (int c = ttid; c < HALF; c += TEAM) {
             const int64_t gj = C0 + c;
             if (gj < n) {
-                PS[I * n + gj] = ts.cc[c][3];   // counter slot of the 8th row tile
-                if (want_min) { PSm[I * n + gj] = ts.cmin[c]; PSj[I * n + gj] = ts.cminj[c]; }
+                const int64_t o = ps_slot(I, gj, n, nbs, G, rows_pad);
+                PS[o] = ts.cc[c][3];   // counter slot of the 8th row tile
+                if (want_min) { PSm[o] = ts.cmin[c]; PSj[o] = ts.cminj[c]; }
             }
         }
     }
 }
 
 // omega[i] = pow2 fold of PS[0..nbs)[i] (complete 1024-wide subtrees, zero
-// padded); round-2 minimum over the blocks (ties -> smaller column).
+// padded); round-2 minimum over the blocks (ties -> smaller column).  With G
+// senders (the sharded pass after its all-to-all) slot (g, b, r) sits at
+// (g * nbs + b) * stride + r and exactly one sender produced each (b, r);
+// the others hold 0 / (inf, INT32_MAX), so the sum over g is exact.
 __global__ void omega_finish_kernel(const double* __restrict__ PS, const double* __restrict__ PSm,
-                                    const int32_t* __restrict__ PSj, int64_t n, int64_t nbs,
-                                    double* __restrict__ omega, int32_t* __restrict__ nn_j,
+                                    const int32_t* __restrict__ PSj, int64_t rows, int64_t nbs, int G,
+                                    int64_t stride, double* __restrict__ omega, int32_t* __restrict__ nn_j,
                                     double* __restrict__ nn_d, int8_t* __restrict__ nn_tie) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= rows) return;
     double slots[40];
     double m = INFINITY;
     int32_t mj = INT32_MAX;
     for (int64_t b = 0; b < nbs; ++b) {
-        double v = PS[b * n + i];
+        double v = PS[b * stride + i];
+        for (int g = 1; g < G; ++g) v = __dadd_rn(v, PS[((int64_t)g * nbs + b) * stride + i]);
         int lvl = 0;
         int64_t t = b;
         while (t & 1) {
@@ -374,9 +393,12 @@ __global__ void omega_finish_kernel(const double* __restrict__ PS, const double*
         }
         slots[lvl] = v;
         if (PSm) {
-            const double x = PSm[b * n + i];
-            const int32_t xj = PSj[b * n + i];
-            if (lex_less(x, xj, m, mj)) { m = x; mj = xj; }
+            for (int g = 0; g < G; ++g) {
+                const int64_t o = ((int64_t)g * nbs + b) * stride + i;
+                const double x = PSm[o];
+                const int32_t xj = PSj[o];
+                if (lex_less(x, xj, m, mj)) { m = x; mj = xj; }
+            }
         }
     }
     double acc = 0.0;
@@ -394,19 +416,58 @@ __global__ void omega_finish_kernel(const double* __restrict__ PS, const double*
     }
 }
 
+__global__ void omega_slots_fill_kernel(double* __restrict__ PS, double* __restrict__ PSm,
+                                        int32_t* __restrict__ PSj, int64_t total) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        PS[e] = 0.0;
+        if (PSm) { PSm[e] = INFINITY; PSj[e] = INT32_MAX; }
+    }
+}
+
 size_t omega_sym_smem() { return sizeof(SymSmem); }
+
+void omega_sym_shard_shape(int64_t n, int G, int64_t* nbs, int64_t* rows_pad) {
+    *nbs = (n + SB - 1) / SB;
+    *rows_pad = G == 1 ? n : (n + G - 1) / G;
+}
+
+// Super-tiles (I, J), I <= J, J in [jlo, jhi) into the slot buffers (layout
+// of ps_slot).  Slots of other ranks' tiles are left to the caller's fill.
+static cudaError_t omega_sym_tiles(const double* X, int64_t n, int d, double sigma, const int32_t* comp,
+                                   int64_t jlo, int64_t jhi, int G, int64_t rows_pad, double* PS,
+                                   double* PSm, int32_t* PSj, cudaStream_t st) {
+    const int64_t nbs = (n + SB - 1) / SB;
+    const int64_t np = nbs * SB;
+    const int dpad = (d + SK - 1) / SK * SK;
+    double* XT = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&XT, (size_t)np * dpad * 8, st);
+    if (e != cudaSuccess) return e;
+    e = launch_transpose_pad(X, n, d, np, dpad, XT, st);
+    if (e != cudaSuccess) return e;
+    const size_t smem = sizeof(SymSmem);
+    e = cudaFuncSetAttribute(omega_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t b0 = jlo * (jlo + 1) / 2;
+    const int64_t ctas = jhi * (jhi + 1) / 2 - b0;
+    if (ctas > 0) {
+        const int pid = prof_begin(PK_OMEGA, st);
+        omega_sym_kernel<<<(unsigned)ctas, STH, smem, st>>>(XT, np, dpad, n, nbs, sigma, 1.0 / sigma, comp,
+                                                            PS, PSm, PSj, b0, G, rows_pad);
+        prof_end(pid, st);
+        note_launch(1);
+    }
+    cudaFreeAsync(XT, st);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, const int32_t* comp,
                              double* omega, int32_t* nn_j, double* nn_d, int8_t* nn_tie,
                              cudaStream_t st) {
     const int64_t nbs = (n + SB - 1) / SB;
-    const int64_t np = nbs * SB;
-    const int dpad = (d + SK - 1) / SK * SK;
-    double *XT = nullptr, *PS = nullptr, *PSm = nullptr;
+    double *PS = nullptr, *PSm = nullptr;
     int32_t* PSj = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&XT, (size_t)np * dpad * 8, st);
-    if (e != cudaSuccess) return e;
-    e = cudaMallocAsync((void**)&PS, (size_t)nbs * n * 8, st);
+    cudaError_t e = cudaMallocAsync((void**)&PS, (size_t)nbs * n * 8, st);
     if (e != cudaSuccess) return e;
     if (comp) {
         e = cudaMallocAsync((void**)&PSm, (size_t)nbs * n * 8, st);
@@ -414,23 +475,38 @@ cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, co
         e = cudaMallocAsync((void**)&PSj, (size_t)nbs * n * 4, st);
         if (e != cudaSuccess) return e;
     }
-    e = launch_transpose_pad(X, n, d, np, dpad, XT, st);
+    e = omega_sym_tiles(X, n, d, sigma, comp, 0, nbs, 1, n, PS, PSm, PSj, st);
     if (e != cudaSuccess) return e;
-    const size_t smem = sizeof(SymSmem);
-    e = cudaFuncSetAttribute(omega_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const int64_t ctas = nbs * (nbs + 1) / 2;
-    const int pid = prof_begin(PK_OMEGA, st);
-    omega_sym_kernel<<<(unsigned)ctas, STH, smem, st>>>(XT, np, dpad, n, nbs, sigma, 1.0 / sigma, comp, PS,
-                                                        PSm, PSj);
-    prof_end(pid, st);
-    omega_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(PS, PSm, PSj, n, nbs, omega, nn_j,
+    omega_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(PS, PSm, PSj, n, nbs, 1, n, omega, nn_j,
                                                                      nn_d, nn_tie);
-    note_launch(2);
-    cudaFreeAsync(XT, st);
+    note_launch(1);
     cudaFreeAsync(PS, st);
     if (PSm) cudaFreeAsync(PSm, st);
     if (PSj) cudaFreeAsync(PSj, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_omega_sym_range(const double* X, int64_t n, int d, double sigma, const int32_t* comp,
+                                   int64_t jlo, int64_t jhi, int G, double* PS, double* PSm, int32_t* PSj,
+                                   cudaStream_t st) {
+    int64_t nbs, rows_pad;
+    omega_sym_shard_shape(n, G, &nbs, &rows_pad);
+    const int64_t total = (int64_t)G * nbs * rows_pad;
+    omega_slots_fill_kernel<<<148 * 8, 256, 0, st>>>(PS, comp ? PSm : nullptr, PSj, total);
+    note_launch(1);
+    return omega_sym_tiles(X, n, d, sigma, comp, jlo, jhi, G, rows_pad, PS, comp ? PSm : nullptr,
+                           comp ? PSj : nullptr, st);
+}
+
+cudaError_t launch_omega_rank_merge(int64_t n, int64_t lo, int64_t hi, int G, const double* PS,
+                                    const double* PSm, const int32_t* PSj, double* omega, int32_t* nn_j,
+                                    double* nn_d, int8_t* nn_tie, cudaStream_t st) {
+    int64_t nbs, rows_pad;
+    omega_sym_shard_shape(n, G, &nbs, &rows_pad);
+    const int64_t rows = hi - lo;
+    omega_finish_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(PS, PSm, PSj, rows, nbs, G, rows_pad,
+                                                                        omega, nn_j, nn_d, nn_tie);
+    note_launch(1);
     return cudaGetLastError();
 }
 

@@ -85,6 +85,15 @@ class Comm:
         self.dist.all_to_all_single(recv, send)
         return recv[:, : hi - lo].contiguous()
 
+    def alltoall_chunks(self, t):
+        """t: (world, ...) contiguous, chunk r for rank r; returns (world, ...)
+        with chunk s = what rank s sent here."""
+        if self.world == 1:
+            return t
+        out = _torch().empty_like(t)
+        self.dist.all_to_all_single(out, t)
+        return out
+
     def allgather_stack(self, stack):
         """Fold stacks of every rank, in rank (= row) order."""
         if self.world == 1:
@@ -214,6 +223,41 @@ class CudaBackend:
         check(self.lib.isoc_omega_mst(_ptr(X), n, d, lo, hi, float(sigma), h, _ptr(out), _ptr(nn_j),
                                       _ptr(nn_d), _ptr(nn_tie), self.stream))
         return out, (nn_j, nn_d, nn_tie)
+
+    def omega_shard_shape(self, n: int, G: int) -> tuple:
+        nbs, rows_pad = ctypes.c_int64(), ctypes.c_int64()
+        check(self.lib.isoc_omega_shard_shape(n, G, ctypes.byref(nbs), ctypes.byref(rows_pad)))
+        return int(nbs.value), int(rows_pad.value)
+
+    def omega_sym_range(self, X, n: int, d: int, jlo: int, jhi: int, sigma: float, G: int, h=None):
+        """This rank's flow subtrees (and, with the MST handle h, round-2
+        minima) per (row, super-block) slot, laid out (G, nbs, rows_pad)
+        by row owner: the send buffers of one all-to-all."""
+        torch = self.torch
+        nbs, rows_pad = self.omega_shard_shape(n, G)
+        shape = (G, nbs, rows_pad)
+        ps = self.empty(shape, torch.float64)
+        psm = self.empty(shape, torch.float64) if h is not None else None
+        psj = self.empty(shape, torch.int32) if h is not None else None
+        check(self.lib.isoc_omega_sym_range(_ptr(X), n, d, jlo, jhi, float(sigma), h, G, _ptr(ps),
+                                             None if psm is None else _ptr(psm),
+                                             None if psj is None else _ptr(psj), self.stream))
+        return ps, psm, psj
+
+    def omega_rank_merge(self, n: int, lo: int, hi: int, G: int, ps, psm=None, psj=None):
+        """Owner side: the G senders' slots for rows [lo, hi) -> (omega, nn)."""
+        torch = self.torch
+        rows = hi - lo
+        out = self.empty((rows,), torch.float64)
+        nn = None
+        if psm is not None:
+            nn = (self.empty((rows,), torch.int32), self.empty((rows,), torch.float64),
+                  self.empty((rows,), torch.int8))
+        check(self.lib.isoc_omega_rank_merge(n, lo, hi, G, _ptr(ps), None if psm is None else _ptr(psm),
+                                             None if psj is None else _ptr(psj), _ptr(out),
+                                             *((None, None, None) if nn is None else tuple(_ptr(t) for t in nn)),
+                                             self.stream))
+        return out, nn
 
     # -- Boruvka ------------------------------------------------------
     def mst_create(self, X, n: int, d: int, lo: int, hi: int):

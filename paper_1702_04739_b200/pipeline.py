@@ -155,6 +155,24 @@ def _sigma_pass(P: _Points, alpha: float, want_nn: bool = True):
     return P.b.sigma_partial(P.X, P.n, P.d, P.lo, P.hi, alpha, want_nn=False)
 
 
+def _omega_pass(P: _Points, sigma: float, h=None):
+    """This rank's omega rows (and, with the MST handle h, the exact round-2
+    minima).  Multi-GPU with the symmetric split: every rank evaluates its
+    super-tile range once, one all-to-all per slot buffer delivers each
+    owner the (row, super-block) subtrees of its rows, and the owner folds
+    them -- bitwise the single-GPU result (each slot has one producer)."""
+    if _sharded_symmetric(P):
+        G = P.comm.world
+        jlo, jhi = P.b.sym_block_range(P.n, P.comm.rank, G)
+        ps, psm, psj = P.b.omega_sym_range(P.X, P.n, P.d, jlo, jhi, sigma, G, h)
+        recv = [None if t is None else P.comm.alltoall_chunks(t) for t in (ps, psm, psj)]
+        del ps, psm, psj
+        return P.b.omega_rank_merge(P.n, P.lo, P.hi, G, *recv)
+    if h is None:
+        return P.b.omega(P.X, P.n, P.d, P.lo, P.hi, sigma), None
+    return P.b.omega_mst(P.X, P.n, P.d, P.lo, P.hi, sigma, h)
+
+
 def _round1_from_sigma(P: _Points) -> bool:
     """Borůvka round 1 from the sigma pass's exact nearest neighbours (default)
     or from the tensor-core filter (ISOC_ROUND1=filter: the symmetric sigma
@@ -206,7 +224,7 @@ def _boruvka(P: _Points, nn=None, sigma: Optional[float] = None) -> tuple:
             comps = _progress(one_round(nn), comps, stats)
         if sigma is not None:
             t0 = time.perf_counter()
-            omega_loc, nn2 = b.omega_mst(P.X, n, P.d, P.lo, P.hi, sigma, h)
+            omega_loc, nn2 = _omega_pass(P, sigma, h)
             if hasattr(b.torch, "cuda") and b.torch.cuda.is_available():
                 b.torch.cuda.synchronize()
             stats["omega_ms"] = (time.perf_counter() - t0) * 1e3
@@ -255,7 +273,7 @@ def node_weights(points, sigma: float, alpha: float = 0.0) -> NodeWeights:
     if alpha < 0:
         raise ValueError(f"alpha must be >= 0, got {alpha}")
     P = _Points(points)
-    om = P.comm.allgather_rows(P.b.omega(P.X, P.n, P.d, P.lo, P.hi, sigma), P.n)
+    om = P.comm.allgather_rows(_omega_pass(P, sigma)[0], P.n)
     if alpha > 0:
         _, _, p_loc = _sigma_pass(P, alpha)
         p = P.comm.allgather_rows(p_loc, P.n).cpu().numpy()

@@ -268,6 +268,83 @@ class EmuBackend:
         self.mst_round_local(h, n)   # exact per-row minima for round 2
         return om, "fused"
 
+    # sharded symmetric omega (pipeline._omega_pass with world > 1): complete
+    # 1024-wide flow subtrees per (row, super-block) into owner-major slots
+    def omega_shard_shape(self, n, G):
+        return -(-n // self.SYM_BLOCK), (n if G == 1 else -(-n // G))
+
+    def omega_sym_range(self, X, n, d, jlo, jhi, sigma, G, h=None):
+        Xn = X.numpy()
+        B = self.SYM_BLOCK
+        nbs, rows_pad = self.omega_shard_shape(n, G)
+        ps = np.zeros((G, nbs, rows_pad))
+        psm = np.full((G, nbs, rows_pad), np.inf)
+        psj = np.full((G, nbs, rows_pad), 2**31 - 1, np.int32)
+        D = orc.distance_rows(Xn, 0, n)
+        F = orc.exp(np.negative(D) / sigma)
+        np.fill_diagonal(F, 0.0)
+        Fp = np.zeros((n, nbs * B))
+        Fp[:, :n] = F
+
+        def slot(b, i):
+            r = i * G // n
+            while n * (r + 1) // G <= i:
+                r += 1
+            while n * r // G > i:
+                r -= 1
+            return r, b, i - n * r // G
+
+        def put(i, b):
+            seg = Fp[i, b * B:(b + 1) * B]
+            while seg.size > 1:
+                seg = seg[0::2] + seg[1::2]
+            s = slot(b, i)
+            ps[s] = seg[0]
+            if h is not None:
+                row = D[i, b * B:min((b + 1) * B, n)].copy()
+                row[h.comp[b * B:b * B + row.size] == h.comp[i]] = np.inf
+                if row.size and np.isfinite(row.min()):
+                    j = int(np.argmin(row))
+                    psm[s], psj[s] = row[j], b * B + j
+
+        for J in range(jlo, jhi):
+            for I in range(J + 1):
+                for i in range(I * B, min((I + 1) * B, n)):
+                    put(i, J)
+                if I < J:
+                    for j in range(J * B, min((J + 1) * B, n)):
+                        put(j, I)
+        t = torch.from_numpy
+        return t(ps), (t(psm) if h is not None else None), (t(psj) if h is not None else None)
+
+    def omega_rank_merge(self, n, lo, hi, G, ps, psm=None, psj=None):
+        P = ps.numpy()
+        nbs = P.shape[1]
+        om = np.empty(hi - lo)
+        nn_j = np.full(hi - lo, -1, np.int32)
+        nn_d = np.full(hi - lo, np.inf)
+        for q in range(hi - lo):
+            v = P[0, :, q].copy()
+            for g in range(1, G):
+                v = v + P[g, :, q]
+            w = np.zeros(1 << max(0, (nbs - 1).bit_length()))
+            w[:nbs] = v
+            while w.size > 1:
+                w = w[0::2] + w[1::2]
+            om[q] = w[0]
+            if psm is not None:
+                best = (np.inf, 2**31 - 1)
+                for g in range(G):
+                    for b in range(nbs):
+                        c = (float(psm[g, b, q]), int(psj[g, b, q]))
+                        best = min(best, c)
+                if best[1] != 2**31 - 1:
+                    nn_j[q], nn_d[q] = best[1], best[0]
+        nn = None
+        if psm is not None:
+            nn = (torch.from_numpy(nn_j), torch.from_numpy(nn_d), torch.zeros(hi - lo, dtype=torch.int8))
+        return torch.from_numpy(om), nn
+
     # Boruvka primitives on the shard's rows (exact per-row minima)
     def mst_create(self, X, n, d, lo, hi):
         return MstState(X.numpy(), n, lo, hi)
@@ -275,16 +352,24 @@ class EmuBackend:
     def mst_round_local(self, h, n, nn=None):
         cmin = np.full(n, NO_KEY, dtype=np.int64)
         h.cand = {}
-        for i in range(h.lo, h.hi):
-            r = orc.distance_rows(h.X, i, i + 1)[0]
-            r[h.comp == h.comp[i]] = np.inf
-            j = int(np.argmin(r))
-            if not np.isfinite(r[j]):
+        if getattr(h, "D", None) is None:
+            h.D = orc.distance_rows(h.X, h.lo, h.hi)
+        R = h.D.copy()
+        R[h.comp[h.lo:h.hi, None] == h.comp[None, :]] = np.inf
+        js = np.argmin(R, axis=1)
+        for q, j in enumerate(js.tolist()):
+            i = h.lo + q
+            if not np.isfinite(R[q, j]):
                 continue
-            h.cand[i] = (r[j], j)
-            key = int(np.float64(r[j]).view(np.int64))
+            h.cand[i] = (R[q, j], j)
+            key = int(np.float64(R[q, j]).view(np.int64))
             c = h.comp[i]
             cmin[c] = min(cmin[c], key)
+        if isinstance(nn, tuple):
+            # minima handed in by a fused pass (sharded omega's round 2)
+            # must be the exact per-row minima recomputed here
+            for i, (w, j) in h.cand.items():
+                assert int(nn[0][i - h.lo]) == j and float(nn[1][i - h.lo]) == w, (i, j, w)
         return torch.from_numpy(cmin)
 
     def mst_round_edges(self, h, cmin):

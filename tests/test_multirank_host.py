@@ -129,3 +129,21 @@ def test_sharded_symmetric_sigma_host_logic(world, oracle_mod):
     assert np.array_equal(r["nn"][1], rows[np.arange(n), j])
     srt = np.sort(rows, axis=1)
     assert np.array_equal(r["nn"][2], (srt[:, 0] == srt[:, 1]).astype(np.int8))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_symmetric_omega_host_logic(world, oracle_mod):
+    """Sharded symmetric omega with fused round 2 (gloo, CPU emulation):
+    owner-major slot buffers, one all-to-all per buffer and the owner-side
+    fold give the oracle's omega bitwise and exact round-2 minima (checked
+    inside the emulated round against a recomputation); the MST is Prim's."""
+    n, d, k = 2100, 3, 4
+    X, _ = oracle_mod.generate_random(n, d, k, 3)
+    r = _run(world, n, d, k)
+    ref_sigma = oracle_mod.auto_sigma(X)
+    tree = oracle_mod.prim_mst(X, ref_sigma)
+    prim_edges = sorted((min(u, int(p)), max(u, int(p))) for u, p in enumerate(tree.parent) if p >= 0)
+    omega, _ = oracle_mod.row_folds(X, ref_sigma)
+    assert r["sigma"] == ref_sigma
+    assert [(a, b) for a, b, _ in r["edges"]] == prim_edges
+    assert np.array_equal(r["omega"].view(np.int64), omega.view(np.int64))
