@@ -13,7 +13,9 @@ import subprocess
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libisoclust_b200.so")
+# ISOC_LIB_PATH: an alternative build of the same library (kernel variants
+# timed side by side by tools/time_passes.py); never a CPU substitute
+LIB_PATH = os.environ.get("ISOC_LIB_PATH") or os.path.join(_HERE, "libisoclust_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 ISOC_OK, ISOC_EINVAL, ISOC_ETYPE, ISOC_EINFEASIBLE, ISOC_ENOMEM, ISOC_ECUDA = range(6)
@@ -91,6 +93,8 @@ SIGNATURES = {
     "isoc_peak_tflops": (ctypes.c_int, [ctypes.c_int, PD]),
     "isoc_div_check": (ctypes.c_int, [ctypes.c_ulonglong, ctypes.c_ulonglong,
                                       ctypes.POINTER(ctypes.c_ulonglong), PD]),
+    "isoc_fastpath_check": (ctypes.c_int, [ctypes.c_ulonglong, ctypes.c_ulonglong,
+                                           ctypes.POINTER(ctypes.c_ulonglong), PD]),
 }
 
 
