@@ -3,6 +3,7 @@ pass and the omega pass with fused round-2 minima -- plus checksums of their
 outputs, so kernel variants (ISOC_LIB_PATH=variants/X.so) can be timed side
 by side and checked for identical results."""
 import hashlib
+import os
 import sys
 
 sys.path.insert(0, '.')
@@ -39,6 +40,10 @@ def digest(*ts):
 for _ in range(reps):
     (stack, nn, _), ms = timed(lambda: pipeline._sigma_pass(P, 0.0))
     print(f"sigma_pass n={n} d={d} ms={ms:.1f} nn={digest(*nn)}", flush=True)
+if os.environ.get("NO_NN"):
+    for _ in range(reps):
+        _, ms = timed(lambda: pipeline._sigma_pass(P, 0.0, want_nn=False))
+        print(f"sigma_pass(no nn) n={n} d={d} ms={ms:.1f}", flush=True)
 sigma = pipeline._sigma_from_stack(P, stack)
 h = b.mst_create(P.X, n, d, 0, n)
 cmin = b.mst_round_local(h, n, nn)
