@@ -161,6 +161,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
     __syncthreads();
     if (team == 1) token_pass(team);     // team 0 takes the first epilogue
     double acc[4][8];
+    int32_t compv = 0;
     // linear pipeline over (ti, tj, kc)
     const int total = TI * TJ * nk;
     sym_load(ts.st[0], XT, np, R0, C0, 0, ttid);
@@ -175,8 +176,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
             if (want_min && ttid < TBM + TBN) {
                 const int64_t g = (ttid < TBM) ? R0 + ti * TBM + ttid : C0 + tj * TBN + (ttid - TBM);
-                const int32_t v = g < n ? comp[g] : (ttid < TBM ? -1 : -2);
-                if (ttid < TBM) ts.comp_r[ttid] = v; else ts.comp_c[ttid - TBM] = v;
+                compv = g < n ? comp[g] : (ttid < TBM ? -1 : -2);
             }
         }
         if (it + 1 < total) {
@@ -187,6 +187,12 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
         asm volatile("cp.async.commit_group;\n" ::);
         asm volatile("cp.async.wait_group 1;\n" ::);
         team_sync(team);
+        // the tile's component ids go to shared memory only now: every thread
+        // of the team has left the previous tile's epilogue (which reads them;
+        // a diagonal tile's epilogue ends without a team barrier)
+        if (kc == 0 && want_min && ttid < TBM + TBN) {
+            if (ttid < TBM) ts.comp_r[ttid] = compv; else ts.comp_c[ttid - TBM] = compv;
+        }
         {
             const SymStage& s = ts.st[it & 1];
 #pragma unroll 4

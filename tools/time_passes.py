@@ -39,7 +39,7 @@ def digest(*ts):
 
 for _ in range(reps):
     (stack, nn, _), ms = timed(lambda: pipeline._sigma_pass(P, 0.0))
-    print(f"sigma_pass n={n} d={d} ms={ms:.1f} nn={digest(*nn)}", flush=True)
+    print(f"sigma_pass n={n} d={d} ms={ms:.1f} nn={digest(*nn)} ties={int(nn[2].sum())} nnj={digest(nn[0])} nnd={digest(nn[1])}", flush=True)
 if os.environ.get("NO_NN"):
     for _ in range(reps):
         _, ms = timed(lambda: pipeline._sigma_pass(P, 0.0, want_nn=False))
