@@ -16,6 +16,7 @@
 // With comp != NULL the same tiles give each row's exact minimum
 // (d, j) over columns in other components: Boruvka round 2 for free.
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -23,10 +24,6 @@
 #include "prof.h"
 
 namespace isoc {
-
-#ifndef OMEGA_FAST
-#define OMEGA_FAST 1
-#endif
 
 constexpr int SB = 1024;      // super-block
 constexpr int TBM = 128;      // tile rows
@@ -231,7 +228,6 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
         const int clim = (int)(n - gcb < 0 ? 0 : (n - gcb > TBN ? TBN : n - gcb));
         const int64_t dd64 = gr0 - gcb;
         const int dd = (int)(dd64 < -TBN - 8 ? -TBN - 8 : (dd64 > TBN + 8 ? TBN + 8 : dd64));
-#if OMEGA_FAST
         {
             bool ok = true;
 #pragma unroll
@@ -250,79 +246,77 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                     for (int j = 0; j < 8; ++j) acc[i][j] = __dsqrt_rn(acc[i][j]);
             }
         }
-#else
+        // Inner patches (warp-uniform): every element is a real off-diagonal
+        // pair, so the minima and flows below skip the per-element masks.
+        const bool inner = __all_sync(0xffffffffu, rlim == 4 && clim == TBN && (dd64 <= -4 || dd64 >= TBN));
+        auto mins_flows = [&](auto chk) {
+            constexpr bool CHK = decltype(chk)::value;
+            if (want_min) {
+                // row minima over the tile's 64 columns (ascending within the
+                // thread, so a strict compare keeps the smaller column); d >= 0,
+                // so the bit patterns order like the values
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = __dsqrt_rn(acc[i][j]);
-#endif
-        if (want_min) {
-            // row minima over the tile's 64 columns (ascending within the
-            // thread, so a strict compare keeps the smaller column); d >= 0,
-            // so the bit patterns order like the values
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int32_t cr = ts.comp_r[rg * 4 + i];
-                uint64_t m = 0x7ff0000000000000ull;
-                int32_t mj = INT32_MAX;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const bool ok = i < rlim && LCOL(j) < clim && ts.comp_c[LCOL(j)] != cr;
-                    const uint64_t bv = (uint64_t)__double_as_longlong(acc[i][j]);
-                    if (ok && bv < m) { m = bv; mj = (int32_t)(gcb + LCOL(j)); }
-                }
-#pragma unroll
-                for (int off = 1; off < 8; off <<= 1) {
-                    const uint64_t om = (uint64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off);
-                    const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
-                    if (om < m || (om == m && oj < mj)) { m = om; mj = oj; }
-                }
-                if (cl == 0) {
-                    const int r = rg * 4 + i;
-                    const double md = __longlong_as_double((long long)m);
-                    double pm = tj == 0 ? INFINITY : ts.rmin[r];
-                    int32_t pj = tj == 0 ? INT32_MAX : ts.rminj[r];
-                    if (lex_less(md, mj, pm, pj)) { pm = md; pj = mj; }
-                    ts.rmin[r] = pm;
-                    ts.rminj[r] = pj;
-                }
-            }
-            // column minima over the thread's rows (ascending), then the warp
-            if (!diag) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int32_t cc = ts.comp_c[LCOL(j)];
+                for (int i = 0; i < 4; ++i) {
+                    const int32_t cr = ts.comp_r[rg * 4 + i];
                     uint64_t m = 0x7ff0000000000000ull;
                     int32_t mj = INT32_MAX;
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const bool ok = i < rlim && LCOL(j) < clim && ts.comp_r[rg * 4 + i] != cc;
+                    for (int j = 0; j < 8; ++j) {
+                        const bool ok = (!CHK || (i < rlim && LCOL(j) < clim)) && ts.comp_c[LCOL(j)] != cr;
                         const uint64_t bv = (uint64_t)__double_as_longlong(acc[i][j]);
-                        if (ok && bv < m) { m = bv; mj = (int32_t)(gr0 + i); }
+                        if (ok && bv < m) { m = bv; mj = (int32_t)(gcb + LCOL(j)); }
                     }
 #pragma unroll
-                    for (int off = 8; off < 32; off <<= 1) {
+                    for (int off = 1; off < 8; off <<= 1) {
                         const uint64_t om = (uint64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off);
                         const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
                         if (om < m || (om == m && oj < mj)) { m = om; mj = oj; }
                     }
-                    if ((lane >> 3) == 0) {
-                        ts.xcm[w][LCOL(j)] = __longlong_as_double((long long)m);
-                        ts.xcj[w][LCOL(j)] = mj;
+                    if (cl == 0) {
+                        const int r = rg * 4 + i;
+                        const double md = __longlong_as_double((long long)m);
+                        double pm = tj == 0 ? INFINITY : ts.rmin[r];
+                        int32_t pj = tj == 0 ? INT32_MAX : ts.rminj[r];
+                        if (lex_less(md, mj, pm, pj)) { pm = md; pj = mj; }
+                        ts.rmin[r] = pm;
+                        ts.rminj[r] = pj;
+                    }
+                }
+                // column minima over the thread's rows (ascending), then the warp
+                if (!diag) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int32_t cc = ts.comp_c[LCOL(j)];
+                        uint64_t m = 0x7ff0000000000000ull;
+                        int32_t mj = INT32_MAX;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const bool ok = (!CHK || (i < rlim && LCOL(j) < clim)) && ts.comp_r[rg * 4 + i] != cc;
+                            const uint64_t bv = (uint64_t)__double_as_longlong(acc[i][j]);
+                            if (ok && bv < m) { m = bv; mj = (int32_t)(gr0 + i); }
+                        }
+#pragma unroll
+                        for (int off = 8; off < 32; off <<= 1) {
+                            const uint64_t om = (uint64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off);
+                            const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
+                            if (om < m || (om == m && oj < mj)) { m = om; mj = oj; }
+                        }
+                        if ((lane >> 3) == 0) {
+                            ts.xcm[w][LCOL(j)] = __longlong_as_double((long long)m);
+                            ts.xcj[w][LCOL(j)] = mj;
+                        }
                     }
                 }
             }
-        }
-        // flows in place (diagonal and padding -> 0)
-#if OMEGA_FAST
-        {
+            // flows in place (diagonal and padding -> 0): x = (-d)/sigma for the
+            // batch, one vote, then the branch-free exp or the table exp
             bool ok = true;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const double x = isoc_div_rs(-acc[i][j], sigma, rs);
-                    const bool valid = i < rlim && LCOL(j) < clim && dd + i != LCOL(j);
+                    const bool valid = !CHK || (i < rlim && LCOL(j) < clim && dd + i != LCOL(j));
                     ok = ok && (!valid || exp_fast_ok(x));
                     acc[i][j] = valid ? x : 0.0;
                 }
@@ -331,29 +325,26 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const bool valid = i < rlim && LCOL(j) < clim && dd + i != LCOL(j);
                         const double f = isoc_exp_fast(acc[i][j], sm.exp_tab);
-                        acc[i][j] = valid ? f : 0.0;
+                        if (CHK) {
+                            const bool valid = i < rlim && LCOL(j) < clim && dd + i != LCOL(j);
+                            acc[i][j] = valid ? f : 0.0;
+                        } else {
+                            acc[i][j] = f;
+                        }
                     }
             } else {
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const bool valid = i < rlim && LCOL(j) < clim && dd + i != LCOL(j);
+                        const bool valid = !CHK || (i < rlim && LCOL(j) < clim && dd + i != LCOL(j));
                         acc[i][j] = valid ? isoc_exp(acc[i][j], sm.exp_tab) : 0.0;
                     }
             }
-        }
-#else
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const bool valid = i < rlim && LCOL(j) < clim && dd + i != LCOL(j);
-                acc[i][j] = valid ? isoc_flow_fast(acc[i][j], sigma, rs, sm.exp_tab) : 0.0;
-            }
-#endif
+        };
+        if (inner) mins_flows(std::false_type{});
+        else mins_flows(std::true_type{});
         // row folds (pow2 tree over the tile's 64 columns): own pairs (level
         // 1), lanes cl^1, cl^2, cl^4 (levels 2-4, one 16-column block per q),
         // own q pairs (levels 5-6); 8 tiles -> the team's 512-column subtree;
