@@ -423,7 +423,7 @@ def main():
             "data": "synthetic (generate_random PCG64 seed 0, Gaussian blobs)",
             "config": {"workload": f"c3 blobs N={n} d={d} k={k}" if args.config == "c3"
                        else f"{args.config} blobs N={n} d={d} k={k}",
-                       "n": n, "d": d, "k": k, "parallelism": f"row-shard x{world}",
+                       "n": n, "d": d, "k": k, "parallelism": (f"symmetric super-tile ranges x{world} (rows owned per rank)" if world > 1 else "one GPU, symmetric super-tiles"),
                        "l2": "inputs larger than L2 (N*d*8 bytes) and an n^2 stream per step"},
             "mst_phase_ms": statistics.median(mst_ms) if mst_ms else None,
             "stage_ms": {kk: round(v, 2) for kk, v in run.timings_ms.items()},
