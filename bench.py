@@ -355,14 +355,18 @@ def main():
     # of 1024; sigma adds 128-wide leaf strips beyond each super-block)
     executed_pairs = {}
     if world == 1:
-        nbs = -(-n // 1024)
+        # sigma: 2048-wide super-blocks of 16 x 16 tiles of 128 (+ a strip of 16
+        # tiles per direction); omega: 1024-wide super-blocks, no strip
+        sb, nt = 2048, 16
+        nbs = -(-n // sb)
         tiles = 0
         for J in range(nbs):
             ext = 1 if J + 1 < nbs else 0
-            tiles += J * (64 + 8 * ext + 8) + (64 + 8 * ext) if n >= 2048 else 0
+            tiles += J * (nt * nt + nt * ext + nt) + (nt * nt + nt * ext) if n >= 2048 else 0
         if n >= 2048:
             executed_pairs["sigma_pass"] = tiles * 128 * 128
-        executed_pairs["omega_pass"] = nbs * (nbs + 1) // 2 * 1024 * 1024
+        nbo = -(-n // 1024)
+        executed_pairs["omega_pass"] = nbo * (nbo + 1) // 2 * 1024 * 1024
     tensor_peak = float(peaks().get("bf16_tflops") or 1590.0)   # fp16 dense = bf16 dense rate
     peak_for = {"sigma_pass": fp64_op_peak, "omega_pass": fp64_op_peak,
                 "boruvka_filter": tensor_peak if use_tc else fp32_peak.value}

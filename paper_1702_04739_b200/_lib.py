@@ -63,6 +63,7 @@ SIGNATURES = {
     "isoc_sigma_partial": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P, P, P, P, P]),
     "isoc_sigma_finish": (ctypes.c_int, [P, I64, PD, P]),
     "isoc_sym_block_range": (ctypes.c_int, [I64, I32, I32, PI64, PI64]),
+    "isoc_omega_block_range": (ctypes.c_int, [I64, I32, I32, PI64, PI64]),
     "isoc_sigma_sym_range": (ctypes.c_int, [P, I64, I32, I64, I64, P, P, P, P, P, P, P]),
     "isoc_sigma_rank_merge": (ctypes.c_int, [P, I64, I32, I64, I64, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "isoc_omega": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P]),
@@ -111,6 +112,8 @@ def load():
                 raise ImportError(f"libisoclust_b200.so missing and build failed: {exc}") from exc
         lib = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("ISOC_LIB_PATH") and not hasattr(lib, name):
+                continue   # an older variant build timed side by side (diagnostics only)
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

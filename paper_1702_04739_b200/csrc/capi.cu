@@ -219,7 +219,13 @@ int isoc_sigma_partial(const double* X, int64_t n, int32_t d, int64_t lo, int64_
 
 int isoc_sym_block_range(int64_t n, int32_t rank, int32_t world, int64_t* jlo, int64_t* jhi) {
     if (n < 1 || world < 1 || rank < 0 || rank >= world) return fail(ISOC_EINVAL, "bad rank/world");
-    sym_block_range(n, rank, world, jlo, jhi);
+    sym_block_range(n, rank, world, jlo, jhi, sigma_sym_block());
+    return ISOC_OK;
+}
+
+int isoc_omega_block_range(int64_t n, int32_t rank, int32_t world, int64_t* jlo, int64_t* jhi) {
+    if (n < 1 || world < 1 || rank < 0 || rank >= world) return fail(ISOC_EINVAL, "bad rank/world");
+    sym_block_range(n, rank, world, jlo, jhi, 1024);
     return ISOC_OK;
 }
 
@@ -228,7 +234,7 @@ int isoc_sigma_sym_range(const double* X, int64_t n, int32_t d, int64_t jlo, int
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
     if (n > (int64_t)INT32_MAX) return fail(ISOC_EINVAL, "n too large");
-    const int64_t nbs = (n + 1023) / 1024;
+    const int64_t nbs = (n + sigma_sym_block() - 1) / sigma_sym_block();
     if (jlo < 0 || jhi > nbs || jlo > jhi) return fail(ISOC_EINVAL, "bad block range [%lld, %lld)", (long long)jlo, (long long)jhi);
     ensure_pool();
     int32_t* flags = nullptr;

@@ -42,7 +42,9 @@ cudaError_t launch_sigma_rank_merge(int64_t rows, int G, const double* pv, const
                                     const int32_t* pc, const double* pm1, const double* pm2, const int32_t* pj,
                                     double* row_vals, uint64_t* row_ids, int32_t* row_cnt, int32_t* flags,
                                     int32_t* nn_j, double* nn_d, int8_t* nn_tie, cudaStream_t st);
-void sym_block_range(int64_t n, int rank, int world, int64_t* jlo, int64_t* jhi);
+int sigma_sym_block();
+// balanced ranges of column super-blocks (I <= J super-tiles) of size `block`
+void sym_block_range(int64_t n, int rank, int world, int64_t* jlo, int64_t* jhi, int block);
 
 // omega_sym.cu
 cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, const int32_t* comp,

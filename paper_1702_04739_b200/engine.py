@@ -169,6 +169,11 @@ class CudaBackend:
         check(self.lib.isoc_sym_block_range(n, rank, world, ctypes.byref(lo), ctypes.byref(hi)))
         return int(lo.value), int(hi.value)
 
+    def omega_block_range(self, n: int, rank: int, world: int) -> tuple:
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        check(self.lib.isoc_omega_block_range(n, rank, world, ctypes.byref(lo), ctypes.byref(hi)))
+        return int(lo.value), int(hi.value)
+
     def sigma_sym_range(self, X, n: int, d: int, jlo: int, jhi: int, want_nn: bool = True):
         """This rank's partial leaf stacks and neighbours for all n rows."""
         torch = self.torch

@@ -163,7 +163,7 @@ def _omega_pass(P: _Points, sigma: float, h=None):
     them -- bitwise the single-GPU result (each slot has one producer)."""
     if _sharded_symmetric(P):
         G = P.comm.world
-        jlo, jhi = P.b.sym_block_range(P.n, P.comm.rank, G)
+        jlo, jhi = P.b.omega_block_range(P.n, P.comm.rank, G)
         ps, psm, psj = P.b.omega_sym_range(P.X, P.n, P.d, jlo, jhi, sigma, G, h)
         recv = [None if t is None else P.comm.alltoall_chunks(t) for t in (ps, psm, psj)]
         del ps, psm, psj

@@ -143,11 +143,12 @@ class EmuBackend:
 
     # sharded symmetric sigma (pipeline._sigma_pass with world > 1): the
     # rank's per-row partial stacks over its column-block range, restated
-    SYM_BLOCK = 1024
+    SYM_BLOCK = 2048      # sigma_sym.cu YB
+    OMEGA_BLOCK = 1024    # omega_sym.cu SB
 
-    def sym_block_range(self, n, rank, world):
+    def sym_block_range(self, n, rank, world, block=None):
         import math
-        nbs = -(-n // self.SYM_BLOCK)
+        nbs = -(-n // (block or self.SYM_BLOCK))
         tot = nbs * (nbs + 1) / 2.0
 
         def bound(k):
@@ -270,12 +271,15 @@ class EmuBackend:
 
     # sharded symmetric omega (pipeline._omega_pass with world > 1): complete
     # 1024-wide flow subtrees per (row, super-block) into owner-major slots
+    def omega_block_range(self, n, rank, world):
+        return self.sym_block_range(n, rank, world, self.OMEGA_BLOCK)
+
     def omega_shard_shape(self, n, G):
-        return -(-n // self.SYM_BLOCK), (n if G == 1 else -(-n // G))
+        return -(-n // self.OMEGA_BLOCK), (n if G == 1 else -(-n // G))
 
     def omega_sym_range(self, X, n, d, jlo, jhi, sigma, G, h=None):
         Xn = X.numpy()
-        B = self.SYM_BLOCK
+        B = self.OMEGA_BLOCK
         nbs, rows_pad = self.omega_shard_shape(n, G)
         ps = np.zeros((G, nbs, rows_pad))
         psm = np.full((G, nbs, rows_pad), np.inf)
