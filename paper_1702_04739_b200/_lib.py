@@ -80,6 +80,7 @@ SIGNATURES = {
     "isoc_tree_from_edges": (ctypes.c_int, [P, P, P, I64, I64, D, P, ctypes.POINTER(P)]),
     "isoc_tree_from_parent": (ctypes.c_int, [P, P, P, I64, I64, P, ctypes.POINTER(P)]),
     "isoc_tree_export": (ctypes.c_int, [P, P, P, P, P, P, PI64, P]),
+    "isoc_tree_root": (ctypes.c_int, [P, PI64]),
     "isoc_tree_set_weights": (ctypes.c_int, [P, P, P, P]),
     "isoc_decide": (ctypes.c_int, [P, D, I64, I32, PI64]),
     "isoc_witness": (ctypes.c_int, [P, I32, I64, P, P, P, P, PD]),

@@ -674,7 +674,7 @@ int isoc_tree_from_parent(const int64_t* parent, const double* flow, const int64
     *out = nullptr;
     if (n < 1) return fail(ISOC_EINVAL, "empty parent array");
     if (n > (int64_t)INT32_MAX - 1) return fail(ISOC_EINVAL, "n too large");
-    if (root < 0 || root >= n) return fail(ISOC_EINVAL, "root does not match the parent array's sentinel");
+    if (root >= n) return fail(ISOC_EINVAL, "root does not match the parent array's sentinel");
     isoc_tree* t = new isoc_tree();
     t->n = n; t->root = root; t->st = (cudaStream_t)stream;
     int rc = tree_alloc(t, n);
@@ -684,20 +684,25 @@ int isoc_tree_from_parent(const int64_t* parent, const double* flow, const int64
     int64_t* lv = nullptr;
     TCK(aalloc(&off, n + 1, st));
     TCK(aalloc(&adj, n, st));
-    TCK(aalloc(&flags, 2, st));
+    TCK(aalloc(&flags, 3, st));
     TCK(aalloc(&lv, 1, st));
     TCK(cudaMemsetAsync(flags, 0, 2 * sizeof(int32_t), st));
+    TCK(cudaMemsetAsync(flags + 2, 0xff, sizeof(int32_t), st));   // found root: -1
     TCK(launch_children_from_parent(parent, child_id, n, root, off, adj, t->child_id_v, flags,
-                                    flags + 1, st));
-    int32_t hf[2] = {0, 0};
-    TCK(cudaMemcpyAsync(hf, flags, 8, cudaMemcpyDeviceToHost, st));
-    const int32_t hflags = hf[0], nroots = hf[1];
+                                    flags + 1, root < 0 ? flags + 2 : nullptr, st));
+    int32_t hf[3] = {0, 0, -1};
+    TCK(cudaMemcpyAsync(hf, flags, 12, cudaMemcpyDeviceToHost, st));
     TCK(cudaStreamSynchronize(st));
-    if (hflags & 2) { tree_free(t); return fail(ISOC_EINVAL, "parent indices out of range"); }
-    if (nroots != 1 || (hflags & 1)) {
+    const int32_t hflags = hf[0], nroots = hf[1];
+    // mst.py:95-103: exactly one sentinel (the given root, when one is given)
+    if (nroots != 1) {
         tree_free(t);
-        return fail(ISOC_EINVAL, "expected exactly one root sentinel matching root, found %d", nroots);
+        return fail(ISOC_EINVAL, "expected exactly one root sentinel, found %d", nroots);
     }
+    if (hflags & 1) { tree_free(t); return fail(ISOC_EINVAL, "root does not match the parent array's sentinel"); }
+    if (hflags & 2) { tree_free(t); return fail(ISOC_EINVAL, "parent indices out of range"); }
+    if (root < 0) root = hf[2];
+    t->root = root;
     TCK(launch_bfs(n, root, 0, off, adj, nullptr, t->bfs, t->pos_of, t->parent_v, t->depth_v,
                    t->child_id_v, t->parent_d, t->pos_parent, t->child_lo, t->child_cnt, t->level_off,
                    t->scratch, lv, st));
@@ -737,6 +742,12 @@ int isoc_tree_export(isoc_tree* t, int64_t* parent, double* parent_flow, int64_t
     if (parent_dist) CK(cudaMemcpyAsync(parent_dist, t->parent_d, n * 8, cudaMemcpyDeviceToHost, t->st));
     CK(cudaStreamSynchronize(t->st));
     if (max_depth) *max_depth = t->levels - 1;
+    return ISOC_OK;
+}
+
+int isoc_tree_root(const isoc_tree* t, int64_t* root) {
+    if (!t || !root) return fail(ISOC_EINVAL, "null tree");
+    *root = t->root;
     return ISOC_OK;
 }
 

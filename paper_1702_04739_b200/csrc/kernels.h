@@ -104,7 +104,8 @@ cudaError_t launch_build_adjacency(const int32_t* eu, const int32_t* ev, const d
                                    int32_t* work, cudaStream_t st);
 cudaError_t launch_children_from_parent(const int64_t* parent, const int64_t* child_id, int64_t n,
                                         int64_t root, int32_t* off, int32_t* adj, int32_t* child_id_v,
-                                        int32_t* flags, int32_t* nroots, cudaStream_t st);
+                                        int32_t* flags, int32_t* nroots, int32_t* found_root,
+                                        cudaStream_t st);
 cudaError_t launch_bfs(int64_t n, int64_t root, int undirected, const int32_t* off,
                        const int32_t* adj, const double* adjd, int32_t* bfs, int32_t* pos_of,
                        int32_t* parent_v, int32_t* depth_v, int32_t* child_id_v, double* parent_d,

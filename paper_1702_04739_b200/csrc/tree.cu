@@ -222,13 +222,14 @@ __global__ void parent_check_kernel(const int64_t* __restrict__ parent,
                                     const int64_t* __restrict__ child_id, int64_t n, int64_t root,
                                     unsigned long long* __restrict__ keys, int32_t* __restrict__ vals,
                                     int32_t* __restrict__ pkeys, int32_t* __restrict__ bad,
-                                    int32_t* __restrict__ nroots) {
+                                    int32_t* __restrict__ nroots, int32_t* __restrict__ found) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= n) return;
     const int64_t p = parent[u];
     if (p == ISOC_NO_VERTEX) {
         atomicAdd(nroots, 1);
-        if (u != root) atomicOr(bad, 1);
+        if (root >= 0 && u != root) atomicOr(bad, 1);
+        if (found) atomicMax(found, (int32_t)u);   // root < 0: the (unique) sentinel
     } else if (p < 0 || p >= n) {
         atomicOr(bad, 2);
     }
@@ -365,7 +366,8 @@ cudaError_t launch_build_adjacency(const int32_t* eu, const int32_t* ev, const d
 
 cudaError_t launch_children_from_parent(const int64_t* parent, const int64_t* child_id, int64_t n,
                                         int64_t root, int32_t* off, int32_t* adj, int32_t* child_id_v,
-                                        int32_t* flags, int32_t* nroots, cudaStream_t st) {
+                                        int32_t* flags, int32_t* nroots, int32_t* found_root,
+                                        cudaStream_t st) {
     unsigned long long *keys = nullptr, *skeys = nullptr;
     int32_t *vals = nullptr, *pkeys = nullptr, *deg = nullptr;
     cudaError_t e;
@@ -377,7 +379,7 @@ cudaError_t launch_children_from_parent(const int64_t* parent, const int64_t* ch
     ACK(cudaMallocAsync((void**)&deg, (size_t)(n + 1) * 4, st));
     cudaMemsetAsync(nroots, 0, sizeof(int32_t), st);
     parent_check_kernel<<<nblk(n, 256), 256, 0, st>>>(parent, child_id, n, root, keys, vals, pkeys,
-                                                       flags, nroots);
+                                                       flags, nroots, found_root);
     int bits = 32;
     while ((int64_t(1) << (bits - 32)) <= n) ++bits;
     size_t tb = 0;

@@ -124,11 +124,30 @@ class CudaBackend:
     def stream(self) -> ctypes.c_void_p:
         return ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
 
+    _STAGE_THREADS = 8
+    _STAGE_MIN = 64 << 20
+
     def to_device(self, x: np.ndarray):
-        t = self.torch.from_numpy(np.ascontiguousarray(x))
-        if not t.is_pinned():
-            t = t.pin_memory()
-        return t.to(self.device, non_blocking=True)
+        """Host array -> HBM through a page-locked staging buffer (torch's
+        caching host allocator); large arrays are staged by several threads
+        (numpy copies release the GIL), then one async H2D copy."""
+        torch = self.torch
+        a = np.ascontiguousarray(x)
+        t = torch.from_numpy(a)
+        if t.is_pinned():
+            return t.to(self.device, non_blocking=True)
+        if a.nbytes < self._STAGE_MIN:
+            return t.pin_memory().to(self.device, non_blocking=True)
+        staged = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        dst = staged.numpy().reshape(-1)
+        src = a.reshape(-1)
+        k = self._STAGE_THREADS
+        step = -(-src.shape[0] // k)
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(k) as ex:
+            list(ex.map(lambda i: np.copyto(dst[i * step:(i + 1) * step], src[i * step:(i + 1) * step]),
+                        range(k)))
+        return staged.to(self.device, non_blocking=True)
 
     def empty(self, shape, dtype):
         return self.torch.empty(shape, dtype=dtype, device=self.device)
@@ -310,16 +329,22 @@ class CudaBackend:
                                              self.stream, ctypes.byref(h)))
         return DeviceTree(self, h, n)
 
-    def tree_from_parent(self, parent: np.ndarray, flows: np.ndarray, root: int,
+    def tree_from_parent(self, parent: np.ndarray, flows: np.ndarray, root: Optional[int],
                          child_id: Optional[np.ndarray] = None) -> "DeviceTree":
+        """root None: the array's unique sentinel, found (and every index
+        validated) on the device; DeviceTree.root holds it."""
         n = parent.shape[0]
         par = self.to_device(np.ascontiguousarray(parent, dtype=np.int64))
         fl = self.to_device(np.ascontiguousarray(flows, dtype=np.float64))
         cid = None if child_id is None else self.to_device(np.ascontiguousarray(child_id, dtype=np.int64))
         h = ctypes.c_void_p()
         check(self.lib.isoc_tree_from_parent(_ptr(par), _ptr(fl), None if cid is None else _ptr(cid),
-                                             n, root, self.stream, ctypes.byref(h)))
-        return DeviceTree(self, h, n)
+                                             n, -1 if root is None else int(root), self.stream, ctypes.byref(h)))
+        dt = DeviceTree(self, h, n)
+        r = ctypes.c_int64()
+        check(self.lib.isoc_tree_root(h, ctypes.byref(r)))
+        dt.root = int(r.value)
+        return dt
 
 
 @dataclass

@@ -307,25 +307,22 @@ def total_distance(tree: RootedTree) -> float:
 
 
 def tree_from_parent_list(parent, parent_flow, root: Optional[int] = None) -> RootedTree:
-    """mst.py:78-125 on the device (sibling ranks by ascending vertex index)."""
+    """mst.py:78-125 on the device (sibling ranks by ascending vertex index).
+
+    The sentinel count, a given root and the index range are validated on the
+    device (isoc_tree_from_parent), raising ValueError like the reference."""
     # inputs are read, never mutated (the device keeps its own copies)
     par = np.ascontiguousarray(parent, dtype=np.int64)
     flows = np.ascontiguousarray(parent_flow, dtype=np.float64)
     n = par.shape[0]
     if par.ndim != 1 or flows.shape != par.shape:
         raise ValueError("parent and parent_flow must be 1-d arrays of equal length")
-    is_root = par == NO_VERTEX
-    nroots = int(np.count_nonzero(is_root))
-    if root is None:
-        if nroots != 1:
-            raise ValueError(f"expected exactly one root sentinel, found {nroots}")
-        root = int(np.argmax(is_root))
-    elif nroots != 1 or not (0 <= root < n) or not bool(is_root[root]):
+    if n == 0:
+        raise ValueError("expected exactly one root sentinel, found 0")
+    if root is not None and not (0 <= int(root) < n):
         raise ValueError("root does not match the parent array's sentinel")
-    if n and (int(par.min()) < NO_VERTEX or int(par.max()) >= n):
-        raise ValueError("parent indices out of range")
     dt = backend().tree_from_parent(par, flows, root)
-    return _rooted_tree_view(dt, root)
+    return _rooted_tree_view(dt, dt.root)
 
 
 def _device_tree(tree: RootedTree) -> DeviceTree:
