@@ -864,18 +864,32 @@ int isoc_witness(isoc_tree* t, int32_t slot, int64_t k, int64_t* labels, int8_t*
     CK(cudaMallocAsync(&cwork, cbytes, st));
     CK(launch_labels(t->code[slot], t->pos_parent, t->bfs, n, t->levels, cut_v, eta_v, lab_v, lab32,
                      work, st));
+    // the label / cut / eta read-back (copy engine) overlaps the cost kernels
+    // (SMs): a side stream waits for the labels, the main stream goes on
+    cudaStream_t side = nullptr;
+    cudaEvent_t ready = nullptr, copied = nullptr;
+    CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, st));
+    CK(cudaStreamWaitEvent(side, ready, 0));
+    if (labels) CK(cudaMemcpyAsync(labels, lab_v, n * 8, cudaMemcpyDeviceToHost, side));
+    if (cut) CK(cudaMemcpyAsync(cut, cut_v, n, cudaMemcpyDeviceToHost, side));
+    if (eta) CK(cudaMemcpyAsync(eta, eta_v, n * 8, cudaMemcpyDeviceToHost, side));
+    CK(cudaEventRecord(copied, side));
     CK(launch_cost(lab32, t->parent_v, t->flow_v, t->omega_v, t->p_v, n, k, cwork, cbytes, sums,
                    miso_d, st));
-    if (labels) CK(cudaMemcpyAsync(labels, lab_v, n * 8, cudaMemcpyDeviceToHost, st));
-    if (cut) CK(cudaMemcpyAsync(cut, cut_v, n, cudaMemcpyDeviceToHost, st));
-    if (eta) CK(cudaMemcpyAsync(eta, eta_v, n * 8, cudaMemcpyDeviceToHost, st));
     if (sparsities && t->spars[slot])
         CK(cudaMemcpyAsync(sparsities, t->spars[slot], k * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(miso, miso_d, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamWaitEvent(st, copied, 0));   // buffers stay alive until the copies are done
     cudaFreeAsync(cut_v, st); cudaFreeAsync(eta_v, st); cudaFreeAsync(lab_v, st);
     cudaFreeAsync(lab32, st); cudaFreeAsync(work, st); cudaFreeAsync(sums, st);
     cudaFreeAsync(miso_d, st); cudaFreeAsync(cwork, st);
     CK(cudaStreamSynchronize(st));
+    cudaEventDestroy(ready);
+    cudaEventDestroy(copied);
+    cudaStreamDestroy(side);
     return ISOC_OK;
 }
 

@@ -55,18 +55,20 @@ __global__ void __launch_bounds__(512) decide_kernel(DecideArgs A) {
     __shared__ int64_t s_off, s_tot;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     const int G = gridDim.x, b = blockIdx.x;
-    const int64_t n = A.n;
-    // working copies (inputs are never mutated)
-    for (int64_t q = (int64_t)b * blockDim.x + tid; q < n; q += (int64_t)G * blockDim.x) {
-        A.om[q] = A.om0[q];
-        A.p[q] = A.p0[q];
-        A.code[q] = 0;
-    }
-    grid_barrier(A.bar);
+    // Inputs are never mutated.  Instead of copying (om, p) to working
+    // arrays per sweep, the deepest level reads om0 / p0 directly and every
+    // fold writes its parents' working values (om0 / p0 plus the children's
+    // contributions), which the next level up reads; code is written for
+    // every decided position and cleared above the level where the sweep
+    // stops.
     int64_t j = 0;
     const double thr = A.thr;
+    int64_t stop_lo = 0;   // positions [0, stop_lo) were never decided
     for (int64_t lv = A.levels - 1; lv >= 0; --lv) {
         const int64_t lo = A.level_off[lv], hi = A.level_off[lv + 1];
+        const bool deepest = lv == A.levels - 1;
+        const double* pv = deepest ? A.p0 : A.p;
+        const double* ov = deepest ? A.om0 : A.om;
         const int64_t W = hi - lo;
         // canonical index c in [0, W) <-> position hi-1-c
         const int64_t cb = W * b / G, ce = W * (b + 1) / G;
@@ -77,7 +79,7 @@ __global__ void __launch_bounds__(512) decide_kernel(DecideArgs A) {
             int8_t cond = 0;
             if (c < ce) {
                 const int64_t pos = hi - 1 - c;
-                const double f = A.f_pos[pos], pw = A.p[pos], ow = A.om[pos];
+                const double f = A.f_pos[pos], pw = pv[pos], ow = ov[pos];
                 const double rhs = __dmul_rn(thr, ow);
                 if (__dadd_rn(f, pw) <= rhs) cond = 1;
                 else if (__dsub_rn(pw, f) < rhs) cond = 2;
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(512) decide_kernel(DecideArgs A) {
             const int64_t e = off + A.excl[pos];
             if (e < need) {
                 if (A.code[pos] == 1)
-                    A.spars[j + e] = __ddiv_rn(__dadd_rn(A.f_pos[pos], A.p[pos]), A.om[pos]);
+                    A.spars[j + e] = __ddiv_rn(__dadd_rn(A.f_pos[pos], pv[pos]), ov[pos]);
             } else {
                 A.code[pos] = 0;
             }
@@ -137,29 +139,25 @@ __global__ void __launch_bounds__(512) decide_kernel(DecideArgs A) {
             const int64_t PW = phi - plo;
             for (int64_t u = plo + (PW * b) / G + tid; u < plo + (PW * (b + 1)) / G; u += blockDim.x) {
                 const int32_t clo = A.child_lo[u], cnt = A.child_cnt[u];
-                double pu = A.p[u], ou = A.om[u];
-                bool touched = false;
+                double pu = A.p0[u], ou = A.om0[u];
                 for (int32_t q = clo + cnt - 1; q >= clo; --q) {
                     const int8_t cd = A.code[q];
                     if (cd == 1 || cd == 3) {
                         pu = __dadd_rn(pu, A.f_pos[q]);
-                        touched = true;
                     } else if (cd == 2) {
-                        ou = __dadd_rn(ou, A.om[q]);
-                        pu = __dadd_rn(pu, A.p[q]);
-                        touched = true;
+                        ou = __dadd_rn(ou, ov[q]);
+                        pu = __dadd_rn(pu, pv[q]);
                     }
                 }
-                if (touched) {
-                    A.p[u] = pu;
-                    A.om[u] = ou;
-                }
+                A.p[u] = pu;
+                A.om[u] = ou;
             }
         }
         j += (tot < need) ? tot : need;
         grid_barrier(A.bar);
-        if (j >= A.k) break;
+        if (j >= A.k) { stop_lo = lo; break; }
     }
+    for (int64_t q = (int64_t)b * blockDim.x + tid; q < stop_lo; q += (int64_t)G * blockDim.x) A.code[q] = 0;
     if (b == 0 && tid == 0) *A.j_out = j;
 }
 
@@ -208,15 +206,14 @@ __global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
     int8_t* code = A.code + kk * n;
     int32_t* excl = A.excl + kk * n;
     int32_t* chunk_cnt = A.chunk_cnt + kk * Gi;
-    for (int64_t q = (int64_t)bi * blockDim.x + tid; q < n; q += (int64_t)Gi * blockDim.x) {
-        om[q] = A.om0[q];
-        pp[q] = A.p0[q];
-        code[q] = 0;
-    }
-    grid_barrier(A.bar);
+    // no working copies: the deepest level reads om0 / p0, every fold writes
+    // its parents' working values (as decide_kernel)
     int64_t j = 0;
     for (int64_t lv = A.levels - 1; lv >= 0; --lv) {
         const int64_t lo = A.level_off[lv], hi = A.level_off[lv + 1];
+        const bool deepest = lv == A.levels - 1;
+        const double* pv = deepest ? A.p0 : pp;
+        const double* ov = deepest ? A.om0 : om;
         const int64_t W = hi - lo;
         const int64_t cb = W * bi / Gi, ce = W * (bi + 1) / Gi;
         const bool active = j < A.k;
@@ -227,7 +224,7 @@ __global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
                 int32_t is_cut = 0;
                 if (c < ce) {
                     const int64_t pos = hi - 1 - c;
-                    const double f = A.f_pos[pos], pw = pp[pos], ow = om[pos];
+                    const double f = A.f_pos[pos], pw = pv[pos], ow = ov[pos];
                     const double rhs = __dmul_rn(thr, ow);
                     int8_t cond;
                     if (__dadd_rn(f, pw) <= rhs) cond = 1;
@@ -284,20 +281,17 @@ __global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
             const int64_t PW = phi - plo;
             for (int64_t u = plo + (PW * bi) / Gi + tid; u < plo + (PW * (bi + 1)) / Gi; u += blockDim.x) {
                 const int32_t clo = A.child_lo[u], cnt = A.child_cnt[u];
-                double pu = pp[u], ou = om[u];
-                bool touched = false;
+                double pu = A.p0[u], ou = A.om0[u];
                 for (int32_t q = clo + cnt - 1; q >= clo; --q) {
                     const int8_t cd = code[q];
                     if (cd == 1 || cd == 3) {
                         pu = __dadd_rn(pu, A.f_pos[q]);
-                        touched = true;
                     } else if (cd == 2) {
-                        ou = __dadd_rn(ou, om[q]);
-                        pu = __dadd_rn(pu, pp[q]);
-                        touched = true;
+                        ou = __dadd_rn(ou, ov[q]);
+                        pu = __dadd_rn(pu, pv[q]);
                     }
                 }
-                if (touched) {
+                {
                     pp[u] = pu;
                     om[u] = ou;
                 }
