@@ -225,8 +225,8 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                 const uint32_t ph = (uint32_t)((t / TC_STAGES) & 1);
                 if (t >= TC_STAGES) mbar_wait(&sm.empty[s], ph ^ 1);
                 mbar_expect_tx(&sm.full[s], 2 * TC_PART);
-                bulk_g2s(sm.B[s][0], img + (t * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
-                bulk_g2s(sm.B[s][1], img + (t * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+                // hi and lo images of a block are adjacent: one 32 KB copy
+                bulk_g2s(sm.B[s][0], img + (t * 2) * (int64_t)TC_PART, 2 * TC_PART, &sm.full[s]);
               } else {
                 // one stage per K atom: both row blocks' A atom and the tile's B atom
                 for (int a = 0; a < KA; ++a, ++q) {

@@ -54,3 +54,7 @@ for _ in range(reps):
     print(f"omega_mst n={n} d={d} ms={ms:.1f} omega={digest(om)} nn={digest(*nn2[:2])}", flush=True)
 b.mst_destroy(h)
 print(f"sigma={sigma!r}")
+if os.environ.get("PLAIN_OMEGA"):
+    for _ in range(reps):
+        om, ms = timed(lambda: b.omega(P.X, n, d, 0, n, sigma))
+        print(f"omega(plain) n={n} d={d} ms={ms:.1f} omega={digest(om)}", flush=True)
