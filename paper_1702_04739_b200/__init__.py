@@ -10,20 +10,36 @@ from ._lib import InfeasibleSubpartitionError
 from .pipeline import (
     ENGINES,
     WORKERS_ENV_VAR,
-    auto_sigma,
+    auto_sigma_points,
     decide,
     extrema,
     minimum_spanning_tree,
-    node_weights,
+    node_weights_points,
     par_decide,
     par_solve_miso,
-    prim_mst,
     resolve_workers,
     run_pipeline,
     solve_miso,
     summarize,
-    total_distance,
     tree_from_parent_list,
+)
+from .stages import (
+    MAX_POINTS,
+    auto_sigma,
+    distance_matrix,
+    exclusive_scan,
+    extract_labels,
+    flow,
+    min_reduce,
+    node_weights,
+    potentials,
+    prim_mst,
+    reverse_bfs_order,
+    subpartition_cost,
+    sum_reduce,
+    total_distance,
+    validate_distance_matrix,
+    vertex_weights,
 )
 from .types import (
     BRACKET_EPS,
@@ -43,9 +59,11 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BRACKET_EPS", "DecisionOutcome", "ENGINES", "Extrema", "InfeasibleSubpartitionError",
-    "MAX_ITERATIONS", "MisoResult", "NO_VERTEX", "NodeWeights", "PipelineRun", "RootedTree",
-    "WORKERS_ENV_VAR", "auto_sigma", "decide", "extrema", "minimum_spanning_tree",
-    "miso_results_equal", "node_weights", "outcomes_equal", "par_decide", "par_solve_miso",
-    "prim_mst", "resolve_workers", "run_pipeline", "solve_miso", "summarize", "total_distance",
-    "tree_from_parent_list", "__version__",
+    "MAX_ITERATIONS", "MAX_POINTS", "MisoResult", "NO_VERTEX", "NodeWeights", "PipelineRun", "RootedTree",
+    "WORKERS_ENV_VAR", "auto_sigma", "auto_sigma_points", "decide", "distance_matrix", "exclusive_scan",
+    "extract_labels", "extrema", "flow", "min_reduce", "minimum_spanning_tree", "miso_results_equal",
+    "node_weights", "node_weights_points", "outcomes_equal", "par_decide", "par_solve_miso", "potentials",
+    "prim_mst", "resolve_workers", "reverse_bfs_order", "run_pipeline", "solve_miso", "subpartition_cost",
+    "sum_reduce", "summarize", "total_distance", "tree_from_parent_list", "validate_distance_matrix",
+    "vertex_weights", "__version__",
 ]

@@ -71,6 +71,17 @@ SIGNATURES = {
     "isoc_omega_shard_shape": (ctypes.c_int, [I64, I32, PI64, PI64]),
     "isoc_omega_sym_range": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, I32, P, P, P, P]),
     "isoc_omega_rank_merge": (ctypes.c_int, [I64, I64, I64, I32, P, P, P, P, P, P, P, P]),
+    "isoc_distance_matrix": (ctypes.c_int, [P, I64, I32, P, P]),
+    "isoc_flow": (ctypes.c_int, [P, I64, D, P, P]),
+    "isoc_vertex_weights_dense": (ctypes.c_int, [P, I64, D, P, P]),
+    "isoc_potentials_dense": (ctypes.c_int, [P, I64, D, P, P]),
+    "isoc_pairwise_sum": (ctypes.c_int, [P, I64, PD, P]),
+    "isoc_validate_distance_matrix": (ctypes.c_int, [P, I64, ctypes.POINTER(ctypes.c_int32), P]),
+    "isoc_mst_dense": (ctypes.c_int, [P, I64, P, P, P, PI64, P]),
+    "isoc_sum_reduce": (ctypes.c_int, [P, I64, PD, P]),
+    "isoc_min_reduce": (ctypes.c_int, [P, I64, PD, PI64, P]),
+    "isoc_exclusive_scan": (ctypes.c_int, [P, I64, P, P]),
+    "isoc_extract_labels": (ctypes.c_int, [P, P, I64, P, P]),
     "isoc_mst_create": (ctypes.c_int, [P, I64, I32, I64, I64, P, ctypes.POINTER(P)]),
     "isoc_mst_round_local": (ctypes.c_int, [P, ctypes.c_int, P, P, P, P]),
     "isoc_mst_round_edges": (ctypes.c_int, [P, P, P]),
@@ -81,6 +92,7 @@ SIGNATURES = {
     "isoc_tree_from_parent": (ctypes.c_int, [P, P, P, I64, I64, P, ctypes.POINTER(P)]),
     "isoc_tree_export": (ctypes.c_int, [P, P, P, P, P, P, PI64, P]),
     "isoc_tree_root": (ctypes.c_int, [P, PI64]),
+    "isoc_tree_cost": (ctypes.c_int, [P, P, I64, PD]),
     "isoc_tree_set_weights": (ctypes.c_int, [P, P, P, P]),
     "isoc_decide": (ctypes.c_int, [P, D, I64, I32, PI64]),
     "isoc_witness": (ctypes.c_int, [P, I32, I64, P, P, P, P, PD]),

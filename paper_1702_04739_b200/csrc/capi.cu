@@ -893,6 +893,32 @@ int isoc_witness(isoc_tree* t, int32_t slot, int64_t k, int64_t* labels, int8_t*
     return ISOC_OK;
 }
 
+__global__ void labels_to_i32_kernel(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)in[i];
+}
+
+int isoc_tree_cost(isoc_tree* t, const int64_t* labels, int64_t k, double* miso) {
+    if (!t || !t->omega_v) return fail(ISOC_EINVAL, "weights not attached");
+    if (k < 1) return fail(ISOC_EINVAL, "no clusters: labels contain no value >= 1");
+    const int64_t n = t->n;
+    cudaStream_t st = t->st;
+    int32_t* lab32 = nullptr;
+    double *sums = nullptr, *miso_d = nullptr;
+    void* cwork = nullptr;
+    const size_t cbytes = cost_work_bytes(n, k);
+    CK(aalloc(&lab32, n, st));
+    CK(aalloc(&sums, 3 * k, st));
+    CK(aalloc(&miso_d, 1, st));
+    CK(cudaMallocAsync(&cwork, cbytes, st));
+    labels_to_i32_kernel<<<blocks(n, 256), 256, 0, st>>>(labels, n, lab32);
+    CK(launch_cost(lab32, t->parent_v, t->flow_v, t->omega_v, t->p_v, n, k, cwork, cbytes, sums, miso_d, st));
+    CK(cudaMemcpyAsync(miso, miso_d, 8, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(lab32, st); cudaFreeAsync(sums, st); cudaFreeAsync(miso_d, st); cudaFreeAsync(cwork, st);
+    CK(cudaStreamSynchronize(st));
+    return ISOC_OK;
+}
+
 void isoc_tree_destroy(isoc_tree* t) {
     if (t) cudaStreamSynchronize(t->st);
     tree_free(t);

@@ -116,6 +116,8 @@ cudaError_t launch_flows(const double* parent_d, const int32_t* parent_v, int64_
 cudaError_t launch_gather_pos(const int32_t* bfs, int64_t n, const double* flow_v,
                               const double* omega_v, const double* p_v, double* f_pos,
                               double* om_pos, double* p_pos, cudaStream_t st);
+cudaError_t launch_pow2_sum(const double* v, int64_t m, double* out, double* tmp, cudaStream_t st);
+cudaError_t launch_min_value(const double* v, int64_t m, double* out, unsigned long long* key, cudaStream_t st);
 cudaError_t launch_extrema(const double* flow_v, int64_t root, const double* omega, const double* p,
                            int64_t n, double* out6, double* tmp, unsigned long long* key,
                            cudaStream_t st);

@@ -342,6 +342,15 @@ static cudaError_t min_value(const double* v, int64_t m, int64_t root, double* o
     return cudaGetLastError();
 }
 
+// plain pow2 zero-padded fold / minimum of a device vector (the stage API's
+// sum_reduce / min_reduce, _primitives.py:69-124)
+cudaError_t launch_pow2_sum(const double* v, int64_t m, double* out, double* tmp, cudaStream_t st) {
+    return pow2_sum<0>(v, m, 0, out, tmp, st);
+}
+cudaError_t launch_min_value(const double* v, int64_t m, double* out, unsigned long long* key, cudaStream_t st) {
+    return min_value<0>(v, m, 0, out, key, st);
+}
+
 // ------------------------------------------------------------- launchers
 cudaError_t launch_build_adjacency(const int32_t* eu, const int32_t* ev, const double* ed,
                                    int64_t n, int32_t* off, int32_t* adj, double* adjd,

@@ -409,6 +409,13 @@ class DeviceTree:
         check(self.b.lib.isoc_decide_batch(self.h, thr.ctypes.data, int(thr.shape[0]), int(k), j.ctypes.data))
         return [int(v) for v in j]
 
+    def cost(self, labels: np.ndarray, k: int) -> float:
+        """subpartition_cost of given labels on this tree's weights."""
+        lab = self.b.to_device(np.ascontiguousarray(labels, dtype=np.int64))
+        miso = ctypes.c_double()
+        check(self.b.lib.isoc_tree_cost(self.h, _ptr(lab), int(k), ctypes.byref(miso)))
+        return float(miso.value)
+
     def shape(self) -> tuple:
         lv, mw = ctypes.c_int64(), ctypes.c_int64()
         check(self.b.lib.isoc_tree_shape(self.h, ctypes.byref(lv), ctypes.byref(mw)))

@@ -259,15 +259,18 @@ def _rooted_tree_view(dt: DeviceTree, root: int) -> RootedTree:
     return LazyRootedTree(dt, root)
 
 
-def auto_sigma(points) -> float:
-    """Mean off-diagonal distance (affinity.py:233-241), matrix-free, bitwise."""
+def auto_sigma_points(points) -> float:
+    """auto_sigma (affinity.py:233-241) from points, matrix-free, bitwise:
+    the mean off-diagonal distance with numpy's pairwise d.sum() order.
+    (stages.auto_sigma takes a distance matrix, as the reference does.)"""
     P = _Points(points)
     stack, _, _ = _sigma_pass(P, 0.0)
     return _sigma_from_stack(P, stack)
 
 
-def node_weights(points, sigma: float, alpha: float = 0.0) -> NodeWeights:
-    """vertex_weights + potentials (affinity.py:175-257) from points."""
+def node_weights_points(points, sigma: float, alpha: float = 0.0) -> NodeWeights:
+    """node_weights (vertex_weights + potentials, affinity.py:175-257) from
+    points, matrix-free.  (stages.node_weights takes a distance matrix.)"""
     if not (sigma > 0):
         raise ValueError(f"sigma must be > 0, got {sigma}")
     if alpha < 0:
@@ -292,18 +295,6 @@ def minimum_spanning_tree(points, sigma: float, root: int = 0) -> RootedTree:
     u, v, w, _, _ = _boruvka(P)
     dt = P.b.tree_from_edges(u, v, w, P.n, root, sigma)
     return _rooted_tree_view(dt, root)
-
-
-# mst.py name of the stage this replaces
-prim_mst = minimum_spanning_tree
-
-
-def total_distance(tree: RootedTree) -> float:
-    """Tree weight (mst.py:184-187): fsum of the exact parent-edge distances."""
-    dt = _device_tree(tree)
-    pdist = dt.export()[6]
-    nonroot = np.flatnonzero(tree.parent != NO_VERTEX)
-    return math.fsum(float(pdist[u]) for u in nonroot)
 
 
 def tree_from_parent_list(parent, parent_flow, root: Optional[int] = None) -> RootedTree:

@@ -14,6 +14,8 @@ REFERENCE_NAMES = [  # isoclust/__init__.py:71-122, the clustering-path subset
     "PipelineRun", "RootedTree", "WORKERS_ENV_VAR", "auto_sigma", "decide", "extrema", "miso_results_equal",
     "node_weights", "outcomes_equal", "par_decide", "par_solve_miso", "prim_mst", "resolve_workers",
     "run_pipeline", "solve_miso", "summarize", "total_distance", "tree_from_parent_list",
+    "distance_matrix", "flow", "vertex_weights", "potentials", "sum_reduce", "min_reduce", "exclusive_scan",
+    "extract_labels", "subpartition_cost", "reverse_bfs_order",
 ]
 
 
