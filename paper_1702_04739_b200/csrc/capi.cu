@@ -586,6 +586,9 @@ struct isoc_tree {
     int8_t* bcode;
     int32_t *bexcl, *bscratch;
     int64_t* bj;
+    // witness read-back overlap (isoc_witness), created on first use
+    cudaStream_t side;
+    cudaEvent_t ev_ready, ev_copied;
 };
 
 static void tree_free(isoc_tree* t) {
@@ -597,6 +600,12 @@ static void tree_free(isoc_tree* t) {
                     t->bthr, t->bcode, t->bexcl, t->bscratch, t->bj};
     for (void* p : ptrs)
         if (p) cudaFreeAsync(p, t->st);
+    if (t->side) {
+        cudaStreamSynchronize(t->side);
+        cudaStreamDestroy(t->side);
+        cudaEventDestroy(t->ev_ready);
+        cudaEventDestroy(t->ev_copied);
+    }
     delete t;
 }
 
@@ -866,11 +875,13 @@ int isoc_witness(isoc_tree* t, int32_t slot, int64_t k, int64_t* labels, int8_t*
                      work, st));
     // the label / cut / eta read-back (copy engine) overlaps the cost kernels
     // (SMs): a side stream waits for the labels, the main stream goes on
-    cudaStream_t side = nullptr;
-    cudaEvent_t ready = nullptr, copied = nullptr;
-    CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    if (!t->side) {
+        CK(cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&t->ev_ready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&t->ev_copied, cudaEventDisableTiming));
+    }
+    cudaStream_t side = t->side;
+    cudaEvent_t ready = t->ev_ready, copied = t->ev_copied;
     CK(cudaEventRecord(ready, st));
     CK(cudaStreamWaitEvent(side, ready, 0));
     if (labels) CK(cudaMemcpyAsync(labels, lab_v, n * 8, cudaMemcpyDeviceToHost, side));
@@ -887,9 +898,6 @@ int isoc_witness(isoc_tree* t, int32_t slot, int64_t k, int64_t* labels, int8_t*
     cudaFreeAsync(lab32, st); cudaFreeAsync(work, st); cudaFreeAsync(sums, st);
     cudaFreeAsync(miso_d, st); cudaFreeAsync(cwork, st);
     CK(cudaStreamSynchronize(st));
-    cudaEventDestroy(ready);
-    cudaEventDestroy(copied);
-    cudaStreamDestroy(side);
     return ISOC_OK;
 }
 

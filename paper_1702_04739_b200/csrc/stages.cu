@@ -200,6 +200,23 @@ __global__ void finite_kernel(const double* __restrict__ v, int64_t m, int32_t* 
 
 inline unsigned nb(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// Stream-ordered scratch freed on every return path.
+struct Scratch {
+    cudaStream_t st;
+    void* ptrs[16];
+    int count = 0;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    template <typename T>
+    cudaError_t alloc(T** p, size_t elems) {
+        cudaError_t e = cudaMallocAsync((void**)p, (elems ? elems : 1) * sizeof(T), st);
+        if (e == cudaSuccess && count < 16) ptrs[count++] = *p;
+        return e;
+    }
+    ~Scratch() {
+        for (int i = 0; i < count; ++i) cudaFreeAsync(ptrs[i], st);
+    }
+};
+
 }  // namespace
 }  // namespace isoc
 
@@ -219,15 +236,15 @@ extern "C" {
 
 int isoc_distance_matrix(const double* X, int64_t n, int32_t d, double* D, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    Scratch S(st);
     if (n < 1 || d < 1) return set_error(ISOC_EINVAL, "need n >= 1 and d >= 1");
     if (n > 65535) return set_error(ISOC_EINVAL, "dense distance matrix limited to 65535 rows");
     const int64_t np = (n + 1023) / 1024 * 1024;
     double* XT = nullptr;
-    SCK(cudaMallocAsync((void**)&XT, (size_t)np * d * 8, st));
+    SCK(S.alloc(&XT, (size_t)np * d));
     SCK(launch_transpose_pad(X, n, d, np, d, XT, st));
     dist_dense_kernel<<<dim3(nb(n, 256), (unsigned)n), 256, 0, st>>>(XT, np, d, n, D);
     note_launch(1);
-    cudaFreeAsync(XT, st);
     SCK(cudaGetLastError());
     return ISOC_OK;
 }
@@ -266,13 +283,14 @@ int isoc_potentials_dense(const double* D, int64_t n, double alpha, double* p, v
 
 int isoc_pairwise_sum(const double* v, int64_t m, double* total_host, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    Scratch S(st);
     if (m < 1) return set_error(ISOC_EINVAL, "pairwise sum of an empty array");
     const int64_t nch = (m + kSumSpan - 1) / kSumSpan;
     FoldStack *stacks = nullptr, *out = nullptr;
     int32_t* flags = nullptr;
-    SCK(cudaMallocAsync((void**)&stacks, (size_t)nch * sizeof(FoldStack), st));
-    SCK(cudaMallocAsync((void**)&out, sizeof(FoldStack), st));
-    SCK(cudaMallocAsync((void**)&flags, 4, st));
+    SCK(S.alloc(&stacks, (size_t)nch));
+    SCK(S.alloc(&out, 1));
+    SCK(S.alloc(&flags, 1));
     SCK(cudaMemsetAsync(flags, 0, 4, st));
     pairwise_chunks_kernel<<<nb(nch, 128), 128, 0, st>>>(v, m, nch, stacks, flags);
     note_launch(1);
@@ -280,7 +298,7 @@ int isoc_pairwise_sum(const double* v, int64_t m, double* total_host, void* stre
     FoldStack* a = stacks;
     int64_t cur = nch;
     FoldStack* tmp = nullptr;
-    if (cur > 1) SCK(cudaMallocAsync((void**)&tmp, (size_t)((cur + 63) / 64) * 2 * sizeof(FoldStack), st));
+    if (cur > 1) SCK(S.alloc(&tmp, (size_t)((cur + 63) / 64) * 2));
     FoldStack* b = tmp;
     FoldStack* c2 = tmp ? tmp + (cur + 63) / 64 : nullptr;
     while (cur > 1) {
@@ -294,8 +312,6 @@ int isoc_pairwise_sum(const double* v, int64_t m, double* total_host, void* stre
     int32_t hf = 0;
     SCK(cudaMemcpyAsync(&hf, flags, 4, cudaMemcpyDeviceToHost, st));
     SCK(cudaStreamSynchronize(st));
-    cudaFreeAsync(stacks, st); cudaFreeAsync(out, st); cudaFreeAsync(flags, st);
-    if (tmp) cudaFreeAsync(tmp, st);
     if (hf || h.overflow) return set_error(ISOC_ECUDA, "pairwise fold stack overflow");
     if (h.count != 1 || h.id[0] != 1) return set_error(ISOC_ECUDA, "pairwise fold did not close (%d)", h.count);
     *total_host = h.value[0];
@@ -304,36 +320,37 @@ int isoc_pairwise_sum(const double* v, int64_t m, double* total_host, void* stre
 
 int isoc_validate_distance_matrix(const double* D, int64_t n, int32_t* flags_host, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    Scratch S(st);
     if (n < 1) return set_error(ISOC_EINVAL, "empty matrix");
     int32_t* flags = nullptr;
-    SCK(cudaMallocAsync((void**)&flags, 4, st));
+    SCK(S.alloc(&flags, 1));
     SCK(cudaMemsetAsync(flags, 0, 4, st));
     validate_kernel<<<dim3(nb(n, 256), (unsigned)n), 256, 0, st>>>(D, n, flags);
     note_launch(1);
     SCK(cudaMemcpyAsync(flags_host, flags, 4, cudaMemcpyDeviceToHost, st));
     SCK(cudaStreamSynchronize(st));
-    cudaFreeAsync(flags, st);
     return ISOC_OK;
 }
 
 int isoc_mst_dense(const double* D, int64_t n, int32_t* eu, int32_t* ev, double* ed, int64_t* ties_host,
                    void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    Scratch S(st);
     if (n < 2) return set_error(ISOC_EINVAL, "need at least 2 points");
     int32_t *comp = nullptr, *cand_j = nullptr, *succ = nullptr, *succ2 = nullptr, *cnt = nullptr;
     double* cand_d = nullptr;
     int8_t *cand_state = nullptr, *cand_tie = nullptr;
     unsigned long long *compD = nullptr, *compE = nullptr;
-    SCK(cudaMallocAsync((void**)&comp, n * 4, st));
-    SCK(cudaMallocAsync((void**)&cand_j, n * 4, st));
-    SCK(cudaMallocAsync((void**)&succ, n * 4, st));
-    SCK(cudaMallocAsync((void**)&succ2, n * 4, st));
-    SCK(cudaMallocAsync((void**)&cnt, 8 * 4, st));
-    SCK(cudaMallocAsync((void**)&cand_d, n * 8, st));
-    SCK(cudaMallocAsync((void**)&cand_state, n, st));
-    SCK(cudaMallocAsync((void**)&cand_tie, n, st));
-    SCK(cudaMallocAsync((void**)&compD, n * 8, st));
-    SCK(cudaMallocAsync((void**)&compE, n * 8, st));
+    SCK(S.alloc(&comp, n));
+    SCK(S.alloc(&cand_j, n));
+    SCK(S.alloc(&succ, n));
+    SCK(S.alloc(&succ2, n));
+    SCK(S.alloc(&cnt, 8));
+    SCK(S.alloc(&cand_d, n));
+    SCK(S.alloc(&cand_state, n));
+    SCK(S.alloc(&cand_tie, n));
+    SCK(S.alloc(&compD, n));
+    SCK(S.alloc(&compE, n));
     SCK(cudaMemsetAsync(cnt, 0, 8 * 4, st));
     iota32_kernel<<<nb(n, 256), 256, 0, st>>>(comp, n);
     int64_t comps = n, rounds = 0;
@@ -351,8 +368,6 @@ int isoc_mst_dense(const double* D, int64_t n, int32_t* eu, int32_t* ev, double*
         comps = c[4];
         if (++rounds > 64) return set_error(ISOC_ECUDA, "Boruvka did not converge");
     }
-    void* ptrs[] = {comp, cand_j, succ, succ2, cnt, cand_d, cand_state, cand_tie, compD, compE};
-    for (void* q : ptrs) cudaFreeAsync(q, st);
     SCK(cudaStreamSynchronize(st));
     if (c[2] != n - 1) return set_error(ISOC_ECUDA, "MST has %d edges, expected %lld", c[2], (long long)(n - 1));
     if (ties_host) *ties_host = c[1];
@@ -361,13 +376,14 @@ int isoc_mst_dense(const double* D, int64_t n, int32_t* eu, int32_t* ev, double*
 
 int isoc_sum_reduce(const double* v, int64_t m, double* out_host, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    Scratch S(st);
     if (m < 1) return set_error(ISOC_EINVAL, "sum_reduce of an empty array");
     double* out = nullptr;
     double* tmp = nullptr;
     int32_t* flags = nullptr;
-    SCK(cudaMallocAsync((void**)&out, 8, st));
-    SCK(cudaMallocAsync((void**)&tmp, (size_t)(m / 1024 + 8) * 8 * 2, st));
-    SCK(cudaMallocAsync((void**)&flags, 4, st));
+    SCK(S.alloc(&out, 1));
+    SCK(S.alloc(&tmp, (size_t)(m / 1024 + 8) * 2));
+    SCK(S.alloc(&flags, 1));
     SCK(cudaMemsetAsync(flags, 0, 4, st));
     finite_kernel<<<148 * 4, 256, 0, st>>>(v, m, flags);
     SCK(launch_pow2_sum(v, m, out, tmp, st));
@@ -375,21 +391,21 @@ int isoc_sum_reduce(const double* v, int64_t m, double* out_host, void* stream) 
     SCK(cudaMemcpyAsync(out_host, out, 8, cudaMemcpyDeviceToHost, st));
     SCK(cudaMemcpyAsync(&hf, flags, 4, cudaMemcpyDeviceToHost, st));
     SCK(cudaStreamSynchronize(st));
-    cudaFreeAsync(out, st); cudaFreeAsync(tmp, st); cudaFreeAsync(flags, st);
     if (hf) return set_error(ISOC_EINVAL, "sum_reduce requires finite values");
     return ISOC_OK;
 }
 
 int isoc_min_reduce(const double* v, int64_t m, double* val_host, int64_t* idx_host, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    Scratch S(st);
     if (m < 1) return set_error(ISOC_EINVAL, "min_reduce of an empty array");
     double* out = nullptr;
     unsigned long long *key = nullptr, *idx = nullptr;
     int32_t* flags = nullptr;
-    SCK(cudaMallocAsync((void**)&out, 8, st));
-    SCK(cudaMallocAsync((void**)&key, 8, st));
-    SCK(cudaMallocAsync((void**)&idx, 8, st));
-    SCK(cudaMallocAsync((void**)&flags, 4, st));
+    SCK(S.alloc(&out, 1));
+    SCK(S.alloc(&key, 1));
+    SCK(S.alloc(&idx, 1));
+    SCK(S.alloc(&flags, 1));
     SCK(cudaMemsetAsync(flags, 0, 4, st));
     SCK(cudaMemsetAsync(idx, 0xff, 8, st));
     finite_kernel<<<148 * 4, 256, 0, st>>>(v, m, flags);
@@ -402,7 +418,6 @@ int isoc_min_reduce(const double* v, int64_t m, double* val_host, int64_t* idx_h
     SCK(cudaMemcpyAsync(&hi, idx, 8, cudaMemcpyDeviceToHost, st));
     SCK(cudaMemcpyAsync(&hf, flags, 4, cudaMemcpyDeviceToHost, st));
     SCK(cudaStreamSynchronize(st));
-    cudaFreeAsync(out, st); cudaFreeAsync(key, st); cudaFreeAsync(idx, st); cudaFreeAsync(flags, st);
     if (hf) return set_error(ISOC_EINVAL, "min_reduce requires finite values");
     *idx_host = (int64_t)hi;
     return ISOC_OK;
@@ -410,13 +425,13 @@ int isoc_min_reduce(const double* v, int64_t m, double* val_host, int64_t* idx_h
 
 int isoc_exclusive_scan(const int64_t* v, int64_t m, int64_t* out, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    Scratch S(st);
     if (m < 1) return ISOC_OK;
     size_t tb = 0;
     SCK(cub::DeviceScan::ExclusiveSum(nullptr, tb, v, out, (int)m, st));
     void* tmp = nullptr;
-    SCK(cudaMallocAsync(&tmp, tb, st));
+    SCK(S.alloc(reinterpret_cast<uint8_t**>(&tmp), tb));
     SCK(cub::DeviceScan::ExclusiveSum(tmp, tb, v, out, (int)m, st));
-    cudaFreeAsync(tmp, st);
     note_launch(1);
     SCK(cudaGetLastError());
     return ISOC_OK;
@@ -424,12 +439,13 @@ int isoc_exclusive_scan(const int64_t* v, int64_t m, int64_t* out, void* stream)
 
 int isoc_extract_labels(const int8_t* cut, const int64_t* eta, int64_t n, int64_t* labels, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    Scratch S(st);
     if (n < 1) return ISOC_OK;
     int64_t *c64 = nullptr, *scan = nullptr;
     int32_t* flags = nullptr;
-    SCK(cudaMallocAsync((void**)&c64, n * 8, st));
-    SCK(cudaMallocAsync((void**)&scan, n * 8, st));
-    SCK(cudaMallocAsync((void**)&flags, 4, st));
+    SCK(S.alloc(&c64, n));
+    SCK(S.alloc(&scan, n));
+    SCK(S.alloc(&flags, 1));
     SCK(cudaMemsetAsync(flags, 0, 4, st));
     cut_to_i64_kernel<<<nb(n, 256), 256, 0, st>>>(cut, n, c64);
     int rc = isoc_exclusive_scan(c64, n, scan, stream);
@@ -439,7 +455,6 @@ int isoc_extract_labels(const int8_t* cut, const int64_t* eta, int64_t n, int64_
     int32_t hf = 0;
     SCK(cudaMemcpyAsync(&hf, flags, 4, cudaMemcpyDeviceToHost, st));
     SCK(cudaStreamSynchronize(st));
-    cudaFreeAsync(c64, st); cudaFreeAsync(scan, st); cudaFreeAsync(flags, st);
     if (hf) return set_error(ISOC_EINVAL, "eta holds an out-of-range vertex");
     return ISOC_OK;
 }
