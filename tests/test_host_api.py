@@ -85,3 +85,37 @@ def test_node_weights_validation():
         pkg.NodeWeights(omega=np.ones(3), p=np.zeros(3), sigma=0.0, alpha=0.0)
     with pytest.raises(ValueError):
         pkg.NodeWeights(omega=np.ones(3), p=np.zeros(3), sigma=1.0, alpha=-1.0)
+
+
+def test_dense_stage_api_validation_before_device_use():
+    """The matrix-taking stage functions raise the reference's errors
+    (affinity.py:84-98, 161-230, _primitives.py:127-145, isoperim.py:164-219)
+    before any device work."""
+    from paper_1702_04739_b200 import stages
+    for bad in (np.zeros((3, 4)), np.zeros((1, 1)), np.ones((3, 3))):
+        with pytest.raises(ValueError):
+            stages._check_matrix_shape(bad)
+    with pytest.raises(ValueError):
+        pkg.vertex_weights(np.zeros((3, 3)), 0.0)
+    with pytest.raises(ValueError):
+        pkg.potentials(np.zeros((3, 3)), -1.0)
+    assert np.array_equal(pkg.potentials(np.zeros((3, 3)), 0.0), np.zeros(3))
+    with pytest.raises(ValueError):
+        pkg.flow(1.0, 0.0)
+    with pytest.raises(ValueError):
+        pkg.flow(np.array([-1.0]), 1.0)
+    with pytest.raises(ValueError):
+        pkg.distance_matrix(np.zeros((10, 2)), max_points=5)
+    with pytest.raises(TypeError):
+        pkg.exclusive_scan(np.array([1.5]))
+    with pytest.raises(ValueError):
+        pkg.exclusive_scan(np.array([-1]))
+    assert pkg.exclusive_scan(np.zeros(0, np.int64)).shape == (0,)
+    with pytest.raises(ValueError):
+        pkg.sum_reduce(np.zeros(0))
+    with pytest.raises(ValueError):
+        pkg.min_reduce(np.zeros((2, 2)))
+    out = DecisionOutcome(feasible=False, clusters_found=1, cut=np.zeros(3, np.int8),
+                          eta=np.full(3, -1, np.int64), cluster_sparsities=[])
+    with pytest.raises(ValueError):
+        pkg.extract_labels(out, 1)
