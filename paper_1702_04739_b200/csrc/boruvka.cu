@@ -732,8 +732,7 @@ cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float
     e = cudaMallocAsync((void**)&pj, (size_t)rows * nchunks * 4, st);
     if (e != cudaSuccess) return e;
     const int pid = prof_begin(PK_RESCAN, st);
-    // one resident wave (2 CTAs per SM): the grid-stride loop balances the items
-    rescan_tile_kernel<<<148 * 2, 256, 0, st>>>(X, n, d, comp, rescan_list, rescan_count, nchunks, pm1,
+    rescan_tile_kernel<<<148 * 3, 256, 0, st>>>(X, n, d, comp, rescan_list, rescan_count, nchunks, pm1,
                                                 pm2, pj);
     rescan_reduce_kernel<<<148, 256, 0, st>>>(rescan_list, rescan_count, lo, nchunks, pm1, pm2, pj,
                                               cand_d, cand_j, cand_tie);
