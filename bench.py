@@ -206,15 +206,21 @@ def tree_phase_bench(args):
     lib = _lib.load()
     lib.isoc_prof_read.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_longlong)]
+    lib.isoc_launch_count.restype = ctypes.c_longlong
     for _ in range(args.warmup):
         res = step()
     torch.cuda.synchronize()
+    sampler = ClockSampler(0)
+    sampler.start()
     lib.isoc_prof_enable(1)
+    l0 = lib.isoc_launch_count()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         res = step()
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
+    launches = lib.isoc_launch_count() - l0
+    clocks = sampler.stop()
     kernels = {}
     for kind, name in enumerate(KIND_NAMES):
         tot = ctypes.c_double()
@@ -222,6 +228,35 @@ def tree_phase_bench(args):
         if lib.isoc_prof_read(kind, ctypes.byref(tot), ctypes.byref(cnt)) == 0 and cnt.value:
             kernels[name] = {"ms_total": tot.value / args.steps, "launches": cnt.value / args.steps}
     lib.isoc_prof_enable(0)
+    # HBM roofline of the decision sweep (~45 algorithmic bytes
+    # per vertex per sweep: f, omega, p in, parent / child ranges, codes and
+    # the parents' folded omega / p out)
+    roofline = None
+    if "decide" in kernels:
+        per_ms = kernels["decide"]["ms_total"] / max(1.0, kernels["decide"]["launches"])
+        achieved = 45.0 * n / (per_ms * 1e-3) / 1e9
+        peak = float(peaks().get("hbm_gbs") or 6536.4)
+        roofline = {"kernel": "decide", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": 1.475e9,
+                    "traffic_unit": "bytes per launch (mean over the 78 sweeps of one step)",
+                    "traffic_source": "profiles/round1_ncu_launches_decide_c5.csv (dram__bytes_read.sum + "
+                                      "dram__bytes_write.sum per decide_kernel launch; mean 1.0 ms, 1.46 TB/s)",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "note": "algorithmic 45 B/vertex x n per sweep (SURVEY 8(d)); sweeps stop at the k-th cut, "
+                            "so the measured DRAM traffic is lower; level-synchronous (grid barriers per level), "
+                            "latency rather than bandwidth bounds it"}
+    # CPU baseline: the oracle's tree phase (reference operation order) on a
+    # 1M-vertex tree of the same generator, per vertex
+    cpu = None
+    if not args.no_cpu_baseline:
+        m = 1_000_000
+        cp, cf, co, cpp = orc.random_tree_instance(m, 0)
+        t1 = time.perf_counter()
+        orc.solve_tree(cp, cf, co, cpp, k)
+        cs = time.perf_counter() - t1
+        cpu = {"value": m / cs, "unit": "vertices/s", "cores": 1, "kind": "port",
+               "sample": f"{m}-vertex random recursive tree (same generator), tree_from_parent_list + extrema "
+                         "+ bisection in oracle/isoc_oracle.c (single thread)"}
     print(json.dumps({
         "metric": "tree-phase vertices/sec (C5: random spanning tree, 50M vertices, k=100)",
         "value": n * args.steps / el, "unit": "vertices/s", "n_gpus": 1, "steps": args.steps,
@@ -229,9 +264,11 @@ def tree_phase_bench(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic random recursive tree (PCG64 seed 0), flows 1-U, omega 2-1.9U, p=0",
         "config": {"workload": f"c5 tree phase N={n} k={k}", "n": n, "k": k},
-        "iterations": res.iterations, "miso": res.miso, "kernels": kernels,
+        "iterations": res.iterations, "miso": res.miso, "kernels": kernels, "roofline": roofline,
+        "cpu_baseline": cpu,
         "e2e": {"value": n * args.steps / el, "unit": "vertices/s",
-                "h2d_bytes_per_step": n * 24, "d2h_bytes_per_step": n * 17}}), flush=True)
+                "h2d_bytes_per_step": n * 24, "d2h_bytes_per_step": n * 17},
+        "gpu_launches": int(launches), "clocks": clocks}), flush=True)
 
 
 def main():
