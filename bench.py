@@ -144,6 +144,29 @@ def cpu_sample(X: np.ndarray, rows: int, threads: int):
     return time.perf_counter() - t0
 
 
+def pkg_generate_random(n, d, k, seed):
+    """The package's generate_random (dataset.py:140-168 semantics)."""
+    from paper_1702_04739_b200 import generate_random
+    return generate_random(n, d, k, seed)
+
+
+def synthetic_tree(n: int, seed: int):
+    """C5 input: random recursive tree drawn vectorised as
+    parent[perm[i]] = perm[floor(U_i * i)], flows 1-U[0,1), omega 2-U[0,1.9),
+    p = 0 (the reference's tests/conftest.py:35-70 distributions)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    parent = np.full(n, -1, dtype=np.int64)
+    perm = rng.permutation(n)
+    if n > 1:
+        i = np.arange(1, n, dtype=np.int64)
+        parent[perm[1:]] = perm[np.minimum((rng.random(n - 1) * i).astype(np.int64), i - 1)]
+    flows = np.zeros(n, dtype=np.float64)
+    nonroot = parent != -1
+    flows[nonroot] = 1.0 - rng.uniform(0.0, 1.0, int(nonroot.sum()))
+    omega = 2.0 - rng.uniform(0.0, 1.9, n)
+    return parent, flows, omega, np.zeros(n, dtype=np.float64)
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -187,12 +210,9 @@ def tree_phase_bench(args):
     import torch
     import paper_1702_04739_b200 as pkg
 
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as orc
-
     n = args.n or 50_000_000
     k = args.k or 100
-    parent, flows, omega, p = orc.random_tree_instance(n, 0)
+    parent, flows, omega, p = synthetic_tree(n, 0)
     w = pkg.NodeWeights(omega=omega, p=p, sigma=1.0, alpha=0.0)
 
     def step():
@@ -249,8 +269,11 @@ def tree_phase_bench(args):
     # 1M-vertex tree of the same generator, per vertex
     cpu = None
     if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as orc
+
         m = 1_000_000
-        cp, cf, co, cpp = orc.random_tree_instance(m, 0)
+        cp, cf, co, cpp = synthetic_tree(m, 0)
         t1 = time.perf_counter()
         orc.solve_tree(cp, cf, co, cpp, k)
         cs = time.perf_counter() - t1
@@ -298,10 +321,7 @@ def main():
     lib.isoc_peak_tflops.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
 
     n, d, k = workload(args)
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as orc
-
-    X, _ = orc.generate_random(n, d, k, 0)
+    X, _ = pkg_generate_random(n, d, k, 0)
     X = np.ascontiguousarray(X)
     Xdev = torch.from_numpy(X).pin_memory().cuda()
     torch.cuda.synchronize()

@@ -7,6 +7,23 @@ labels, and runs every arithmetic stage as hand-written sm_100a CUDA kernels
 behind the C ABI in include/isoclust_b200.h (libisoclust_b200.so).
 """
 from ._lib import InfeasibleSubpartitionError
+from .harness import (
+    BENCH_CSV_HEADER,
+    BenchRecord,
+    DataFormatError,
+    DepthSchedule,
+    WorkerPool,
+    benchmark,
+    class_count,
+    generate_random,
+    load_labels,
+    load_points,
+    misclassification_rate,
+    save_labels,
+    save_points,
+    standardize,
+    write_bench_csv,
+)
 from .pipeline import (
     ENGINES,
     WORKERS_ENV_VAR,
@@ -26,6 +43,7 @@ from .pipeline import (
 from .stages import (
     MAX_POINTS,
     auto_sigma,
+    brute_force_miso,
     distance_matrix,
     exclusive_scan,
     extract_labels,
@@ -58,9 +76,12 @@ from .types import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "BENCH_CSV_HEADER", "BenchRecord", "DataFormatError", "DepthSchedule", "WorkerPool", "benchmark",
+    "class_count", "generate_random", "load_labels", "load_points", "misclassification_rate", "save_labels",
+    "save_points", "standardize", "write_bench_csv",
     "BRACKET_EPS", "DecisionOutcome", "ENGINES", "Extrema", "InfeasibleSubpartitionError",
     "MAX_ITERATIONS", "MAX_POINTS", "MisoResult", "NO_VERTEX", "NodeWeights", "PipelineRun", "RootedTree",
-    "WORKERS_ENV_VAR", "auto_sigma", "auto_sigma_points", "decide", "distance_matrix", "exclusive_scan",
+    "WORKERS_ENV_VAR", "auto_sigma", "auto_sigma_points", "brute_force_miso", "decide", "distance_matrix", "exclusive_scan",
     "extract_labels", "extrema", "flow", "min_reduce", "minimum_spanning_tree", "miso_results_equal",
     "node_weights", "node_weights_points", "outcomes_equal", "par_decide", "par_solve_miso", "potentials",
     "prim_mst", "resolve_workers", "reverse_bfs_order", "run_pipeline", "solve_miso", "subpartition_cost",

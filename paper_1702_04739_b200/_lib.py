@@ -82,6 +82,7 @@ SIGNATURES = {
     "isoc_min_reduce": (ctypes.c_int, [P, I64, PD, PI64, P]),
     "isoc_exclusive_scan": (ctypes.c_int, [P, I64, P, P]),
     "isoc_extract_labels": (ctypes.c_int, [P, P, I64, P, P]),
+    "isoc_brute_force_miso": (ctypes.c_int, [P, P, P, P, I32, I32, PI64, PD, P]),
     "isoc_mst_create": (ctypes.c_int, [P, I64, I32, I64, I64, P, ctypes.POINTER(P)]),
     "isoc_mst_round_local": (ctypes.c_int, [P, ctypes.c_int, P, P, P, P]),
     "isoc_mst_round_edges": (ctypes.c_int, [P, P, P]),

@@ -10,10 +10,13 @@
 //                            edge set as Prim for distinct distances)
 //   sum_reduce / min_reduce / exclusive_scan  _primitives.py:62-159
 //   extract_labels           isoperim.py:164-181
+//   brute_force_miso         isoperim.py:324-390 (exhaustive labelling search)
 // The matrix-free pipeline never builds these n^2 arrays; these entry points
 // serve callers of the stage API that hold a distance matrix (the reference
 // caps those at n <= 46,340).
+#include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -196,6 +199,88 @@ __global__ void argmin_index_kernel(const double* __restrict__ v, int64_t m, con
 __global__ void finite_kernel(const double* __restrict__ v, int64_t m, int32_t* __restrict__ flags) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         if (!isfinite(v[i])) atomicOr(flags, 1);
+}
+
+// brute_force_miso (isoperim.py:324-390): labelling code c in [0, (k+1)^n)
+// puts vertex v in cluster digit_v(c) (base k+1, vertex 0 least
+// significant).  Per cluster, mass and potential accumulate in ascending
+// vertex order and the boundary in ascending child order (the sequential
+// order of the reference's 0/1-indicator dot products; a product by 0 or 1
+// is exact).  worst = max(0, max_c sparsity_c); a code leaving a cluster
+// empty is infeasible (+inf).  PASS 0 takes the minimum worst as its bit
+// pattern (nonnegative doubles order as unsigned integers); PASS 1 the
+// smallest code attaining it (np.argmin keeps the first, isoperim.py:380).
+constexpr int BF_MAXN = 12;
+
+template <int PASS>
+__global__ void __launch_bounds__(256) brute_force_kernel(const int32_t* __restrict__ parent,
+                                                          const double* __restrict__ flow,
+                                                          const double* __restrict__ omega,
+                                                          const double* __restrict__ pot, int n, int k,
+                                                          uint32_t total, unsigned long long* best_bits,
+                                                          unsigned long long* best_code) {
+    __shared__ int32_t s_par[BF_MAXN];
+    __shared__ double s_flow[BF_MAXN], s_om[BF_MAXN], s_p[BF_MAXN];
+    if (threadIdx.x < n) {
+        s_par[threadIdx.x] = parent[threadIdx.x];
+        s_flow[threadIdx.x] = flow[threadIdx.x];
+        s_om[threadIdx.x] = omega[threadIdx.x];
+        s_p[threadIdx.x] = pot[threadIdx.x];
+    }
+    __syncthreads();
+    const uint32_t base = (uint32_t)k + 1;
+    const unsigned long long target = PASS ? *best_bits : 0ull;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t rounds = (total + stride - 1) / stride;
+    for (uint32_t r = 0; r < rounds; ++r) {
+        const uint32_t code = r * stride + blockIdx.x * blockDim.x + threadIdx.x;
+        unsigned long long bits = ~0ull;
+        if (code < total) {
+            int dig[BF_MAXN];
+            uint32_t c = code;
+#pragma unroll
+            for (int v = 0; v < BF_MAXN; ++v) {
+                dig[v] = (int)(c % base);
+                c /= base;
+            }
+            double mass[BF_MAXN + 1], bnd[BF_MAXN + 1], pp[BF_MAXN + 1];
+            int cnt[BF_MAXN + 1];
+            for (int q = 0; q <= k; ++q) mass[q] = bnd[q] = pp[q] = 0.0, cnt[q] = 0;
+            for (int v = 0; v < n; ++v) {
+                const int a = dig[v];
+                mass[a] = __dadd_rn(mass[a], s_om[v]);
+                pp[a] = __dadd_rn(pp[a], s_p[v]);
+                cnt[a] += 1;
+                const int w = s_par[v];
+                if (w >= 0) {
+                    const int b = dig[w];
+                    if (a != b) {
+                        bnd[a] = __dadd_rn(bnd[a], s_flow[v]);
+                        bnd[b] = __dadd_rn(bnd[b], s_flow[v]);
+                    }
+                }
+            }
+            double worst = 0.0;
+            bool feasible = true;
+            for (int q = 1; q <= k; ++q) {
+                feasible &= cnt[q] > 0;
+                const double sp = __ddiv_rn(__dadd_rn(bnd[q], pp[q]), mass[q]);
+                worst = sp > worst ? sp : worst;
+            }
+            if (!feasible) worst = __longlong_as_double(0x7ff0000000000000ll);
+            bits = (unsigned long long)__double_as_longlong(worst);
+        }
+        if (PASS == 0) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+                bits = other < bits ? other : bits;
+            }
+            if ((threadIdx.x & 31) == 0 && bits != ~0ull) atomicMin(best_bits, bits);
+        } else if (code < total && bits == target) {
+            atomicMin(best_code, (unsigned long long)code);
+        }
+    }
 }
 
 inline unsigned nb(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -434,6 +519,40 @@ int isoc_exclusive_scan(const int64_t* v, int64_t m, int64_t* out, void* stream)
     SCK(cub::DeviceScan::ExclusiveSum(tmp, tb, v, out, (int)m, st));
     note_launch(1);
     SCK(cudaGetLastError());
+    return ISOC_OK;
+}
+
+int isoc_brute_force_miso(const int32_t* parent, const double* flow, const double* omega, const double* p,
+                          int32_t n, int32_t k, int64_t* code_host, double* worst_host, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch S(st);
+    if (n < 1 || n > BF_MAXN) return set_error(ISOC_EINVAL, "brute force supports 1 <= n <= %d, got %d", BF_MAXN, n);
+    if (k < 1) return set_error(ISOC_EINVAL, "k must be >= 1, got %d", k);
+    if (k > n)
+        return set_error(ISOC_EINFEASIBLE, "no feasible labeling: k=%d clusters require k <= n=%d vertices", k, n);
+    double total = 1.0;
+    for (int v = 0; v < n; ++v) total *= (double)(k + 1);
+    if (total > (double)(1 << 26))
+        return set_error(ISOC_EINVAL, "enumeration of %.0f labelings exceeds the supported size", total);
+    unsigned long long *bits = nullptr, *code = nullptr;
+    SCK(S.alloc(&bits, 1));
+    SCK(S.alloc(&code, 1));
+    SCK(cudaMemsetAsync(bits, 0xff, 8, st));
+    SCK(cudaMemsetAsync(code, 0xff, 8, st));
+    const uint32_t tot = (uint32_t)total;
+    const unsigned grid = (unsigned)std::min<int64_t>(148 * 8, ((int64_t)tot + 255) / 256);
+    brute_force_kernel<0><<<grid, 256, 0, st>>>(parent, flow, omega, p, n, k, tot, bits, code);
+    brute_force_kernel<1><<<grid, 256, 0, st>>>(parent, flow, omega, p, n, k, tot, bits, code);
+    note_launch(2);
+    SCK(cudaGetLastError());
+    unsigned long long hb = 0, hc = 0;
+    SCK(cudaMemcpyAsync(&hb, bits, 8, cudaMemcpyDeviceToHost, st));
+    SCK(cudaMemcpyAsync(&hc, code, 8, cudaMemcpyDeviceToHost, st));
+    SCK(cudaStreamSynchronize(st));
+    double w;
+    memcpy(&w, &hb, 8);
+    *worst_host = w;
+    *code_host = (hc == ~0ull || !(w < __builtin_inf())) ? -1 : (int64_t)hc;
     return ISOC_OK;
 }
 

@@ -201,7 +201,8 @@ def sum_reduce(values, pool=None) -> float:
         raise ValueError("sum_reduce of an empty array")
     b = backend()
     out = ctypes.c_double()
-    check(b.lib.isoc_sum_reduce(_ptr(b.to_device(v)), v.size, ctypes.byref(out), b.stream))
+    dv = b.to_device(v)
+    check(b.lib.isoc_sum_reduce(_ptr(dv), v.size, ctypes.byref(out), b.stream))
     return float(out.value)
 
 
@@ -214,7 +215,8 @@ def min_reduce(values) -> tuple[float, int]:
         raise ValueError("min_reduce of an empty array")
     b = backend()
     val, idx = ctypes.c_double(), ctypes.c_int64()
-    check(b.lib.isoc_min_reduce(_ptr(b.to_device(v)), v.size, ctypes.byref(val), ctypes.byref(idx), b.stream))
+    dv = b.to_device(v)
+    check(b.lib.isoc_min_reduce(_ptr(dv), v.size, ctypes.byref(val), ctypes.byref(idx), b.stream))
     return float(val.value), int(idx.value)
 
 
@@ -271,3 +273,41 @@ def subpartition_cost(labels, tree: RootedTree, weights: NodeWeights) -> float:
     from .pipeline import _attach
     dt = _attach(tree, weights)
     return dt.cost(lab, k)
+
+
+def brute_force_miso(tree: RootedTree, weights: NodeWeights, k: int):
+    """isoperim.py:324-390: exhaustive search over every labelling of the
+    vertices into {0, 1..k} (clusters need not be connected), for tiny
+    instances (n <= 12, at most 2^26 labellings).  The enumeration runs on
+    the device (brute_force_kernel, one labelling per thread); the winner is
+    the smallest labelling code with the minimum worst sparsity, and miso is
+    its exact cost recomputed by subpartition_cost, as in the reference."""
+    from .pipeline import _validate_k
+    from .types import MisoResult
+
+    _validate_k(k)
+    if tree.n != weights.n:
+        raise ValueError(f"tree has {tree.n} vertices but weights have {weights.n}")
+    n = tree.n
+    if n > 12:
+        raise ValueError(f"brute force supports n <= 12, got {n}")
+    if k > n:
+        from ._lib import InfeasibleSubpartitionError
+        raise InfeasibleSubpartitionError(
+            f"no feasible labeling: k={k} clusters require k <= n={n} vertices")
+    if (k + 1) ** n > 1 << 26:
+        raise ValueError(f"enumeration of {(k + 1) ** n} labelings exceeds the supported size")
+    parent = np.where(np.asarray(tree.parent) == NO_VERTEX, -1, np.asarray(tree.parent))
+    b = backend()
+    code, worst = ctypes.c_int64(), ctypes.c_double()
+    bufs = (_dev(parent, np.int32), _dev(tree.parent_flow, np.float64), _dev(weights.omega, np.float64),
+            _dev(weights.p, np.float64))   # held until the call returns
+    check(b.lib.isoc_brute_force_miso(*map(_ptr, bufs), n, int(k), ctypes.byref(code), ctypes.byref(worst),
+                                      b.stream))
+    if code.value < 0:
+        from ._lib import InfeasibleSubpartitionError
+        raise InfeasibleSubpartitionError(f"no feasible labeling found by enumeration (n={n}, k={k})")
+    labels = (code.value // (k + 1) ** np.arange(n, dtype=np.int64)) % (k + 1)
+    exact = subpartition_cost(labels, tree, weights)
+    return MisoResult(miso=exact, labels=labels.astype(np.int64), outcome=None, iterations=0,
+                      alpha_final=exact, beta_final=exact, trace=[])
