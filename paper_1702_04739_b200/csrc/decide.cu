@@ -50,17 +50,72 @@ struct DecideArgs {
     unsigned int* bar;
 };
 
-__global__ void __launch_bounds__(512) decide_kernel(DecideArgs A) {
-    __shared__ int32_t warp_tot[16];
-    __shared__ int64_t s_off, s_tot;
+constexpr int DK_MAXG = 1024;  // chunk counts live in scratch[0, 1024)
+#ifndef DK_UA
+#define DK_UA 2   // phase A: consecutive elements per thread per pass
+#endif
+#ifndef DK_UF
+#define DK_UF 2   // fold: parents per thread per pass
+#endif
+#ifndef DK_MINB
+#define DK_MINB 2 // resident CTAs per SM the register budget is sized for
+#endif
+
+// Exclusive prefix of the G chunk cut counts into s_pre[0..G] (s_pre[G] =
+// level total), computed by every CTA.
+__device__ __forceinline__ void chunk_prefix(const int32_t* __restrict__ cnt, int G, int32_t* s_pre,
+                                             int32_t* warp_tot) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int per = (G + blockDim.x - 1) / blockDim.x;   // <= 2 for G <= 1024
+    int32_t v[2] = {0, 0};
+    int32_t sum = 0;
+    for (int i = 0; i < per; ++i) {
+        const int q = tid * per + i;
+        v[i] = q < G ? ((volatile const int32_t*)cnt)[q] : 0;
+        sum += v[i];
+    }
+    int32_t x = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int32_t t = lane < nw ? warp_tot[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < nw) warp_tot[lane] = t;
+    }
+    __syncthreads();
+    int32_t e = (wid > 0 ? warp_tot[wid - 1] : 0) + x - sum;
+    for (int i = 0; i < per; ++i) {
+        const int q = tid * per + i;
+        if (q <= G) s_pre[q] = e;
+        e += v[i];
+    }
+    if (tid == blockDim.x - 1 && tid * per + per <= G) s_pre[G] = e;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(512, DK_MINB) decide_kernel(DecideArgs A) {
+    __shared__ int32_t warp_tot[16];
+    __shared__ int32_t s_pre[DK_MAXG + 1];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int bd = blockDim.x;
     const int G = gridDim.x, b = blockIdx.x;
     // Inputs are never mutated.  Instead of copying (om, p) to working
     // arrays per sweep, the deepest level reads om0 / p0 directly and every
     // fold writes its parents' working values (om0 / p0 plus the children's
     // contributions), which the next level up reads; code is written for
     // every decided position and cleared above the level where the sweep
-    // stops.
+    // stops.  Per level two grid barriers: A (conditions + chunk-local cut
+    // ranks) | prefix of the chunk counts in every CTA, then the parents'
+    // fold, which also commits each child (the reference's stop at the k-th
+    // cut: committed iff fewer than k - j cuts precede it in canonical
+    // order) | next level.
     int64_t j = 0;
     const double thr = A.thr;
     int64_t stop_lo = 0;   // positions [0, stop_lo) were never decided
@@ -69,27 +124,38 @@ __global__ void __launch_bounds__(512) decide_kernel(DecideArgs A) {
         const bool deepest = lv == A.levels - 1;
         const double* pv = deepest ? A.p0 : A.p;
         const double* ov = deepest ? A.om0 : A.om;
-        const int64_t W = hi - lo;
-        // canonical index c in [0, W) <-> position hi-1-c
-        const int64_t cb = W * b / G, ce = W * (b + 1) / G;
-        int64_t carry = 0;
-        for (int64_t base = cb; base < ce; base += blockDim.x) {
-            const int64_t c = base + tid;
-            int32_t is_cut = 0;
-            int8_t cond = 0;
-            if (c < ce) {
-                const int64_t pos = hi - 1 - c;
-                const double f = A.f_pos[pos], pw = pv[pos], ow = ov[pos];
-                const double rhs = __dmul_rn(thr, ow);
-                if (__dadd_rn(f, pw) <= rhs) cond = 1;
-                else if (__dsub_rn(pw, f) < rhs) cond = 2;
-                else cond = 3;
-                is_cut = cond == 1;
-                A.code[pos] = cond;  // provisional; cleared in B if not committed
-            }
-            int32_t x = is_cut;
+        const uint32_t W = (uint32_t)(hi - lo);
+        // canonical index c in [0, W) <-> position hi-1-c; chunk b = [b*CH, (b+1)*CH)
+        const uint32_t CH = (W + G - 1) / G;
+        const uint32_t cb = min(W, (uint32_t)b * CH), ce = min(W, cb + CH);
+        int32_t carry = 0;
+        for (uint32_t base = cb; base < ce; base += DK_UA * bd) {
+            const uint32_t c0 = base + DK_UA * tid;
+            double f[DK_UA], pw[DK_UA], ow[DK_UA];
+#pragma unroll
+            for (int i = 0; i < DK_UA; ++i)
+                if (c0 + i < ce) {
+                    const int64_t pos = hi - 1 - (c0 + i);
+                    f[i] = A.f_pos[pos];
+                    pw[i] = pv[pos];
+                    ow[i] = ov[pos];
+                }
+            int32_t cuts = 0;
+            uint32_t cutmask = 0;
+#pragma unroll
+            for (int i = 0; i < DK_UA; ++i)
+                if (c0 + i < ce) {
+                    const double rhs = __dmul_rn(thr, ow[i]);
+                    int8_t cond;
+                    if (__dadd_rn(f[i], pw[i]) <= rhs) cond = 1;
+                    else if (__dsub_rn(pw[i], f[i]) < rhs) cond = 2;
+                    else cond = 3;
+                    A.code[hi - 1 - (c0 + i)] = cond;  // provisional; the fold clears it if not committed
+                    if (cond == 1) { cutmask |= 1u << i; ++cuts; }
+                }
+            int32_t x = cuts;
             for (int o = 1; o < 32; o <<= 1) {
-                int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
             if (lane == 31) warp_tot[wid] = x;
@@ -97,60 +163,104 @@ __global__ void __launch_bounds__(512) decide_kernel(DecideArgs A) {
             if (wid == 0) {
                 int32_t t = lane < nw ? warp_tot[lane] : 0;
                 for (int o = 1; o < 32; o <<= 1) {
-                    int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                    const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
                     if (lane >= o) t += y;
                 }
                 if (lane < nw) warp_tot[lane] = t;
             }
             __syncthreads();
-            const int32_t wpre = wid > 0 ? warp_tot[wid - 1] : 0;
-            if (c < ce) A.excl[hi - 1 - c] = (int32_t)(carry + wpre + x - is_cut);
+            int32_t e = carry + (wid > 0 ? warp_tot[wid - 1] : 0) + x - cuts;
+#pragma unroll
+            for (int i = 0; i < DK_UA; ++i)
+                if (c0 + i < ce) {
+                    A.excl[hi - 1 - (c0 + i)] = e;
+                    e += (cutmask >> i) & 1;
+                }
             carry += warp_tot[nw - 1];
             __syncthreads();
         }
-        if (tid == 0) A.chunk_cnt[b] = (int32_t)carry;
+        if (tid == 0) A.chunk_cnt[b] = carry;
         grid_barrier(A.bar);
-        if (tid == 0) {
-            int64_t pre = 0, tot = 0;
-            for (int q = 0; q < G; ++q) {
-                const int64_t s = A.chunk_cnt[q];
-                if (q < b) pre += s;
-                tot += s;
-            }
-            s_off = pre;
-            s_tot = tot;
-        }
-        __syncthreads();
+        chunk_prefix(A.chunk_cnt, G, s_pre, warp_tot);
         const int64_t need = A.k - j;
-        const int64_t off = s_off, tot = s_tot;
-        for (int64_t c = cb + tid; c < ce; c += blockDim.x) {
-            const int64_t pos = hi - 1 - c;
-            const int64_t e = off + A.excl[pos];
-            if (e < need) {
-                if (A.code[pos] == 1)
-                    A.spars[j + e] = __ddiv_rn(__dadd_rn(A.f_pos[pos], pv[pos]), ov[pos]);
-            } else {
-                A.code[pos] = 0;
-            }
-        }
-        grid_barrier(A.bar);
+        const int64_t tot = s_pre[G];
         if (lv > 0) {
-            const int64_t plo = A.level_off[lv - 1], phi = lo;
-            const int64_t PW = phi - plo;
-            for (int64_t u = plo + (PW * b) / G + tid; u < plo + (PW * (b + 1)) / G; u += blockDim.x) {
-                const int32_t clo = A.child_lo[u], cnt = A.child_cnt[u];
-                double pu = A.p0[u], ou = A.om0[u];
-                for (int32_t q = clo + cnt - 1; q >= clo; --q) {
-                    const int8_t cd = A.code[q];
-                    if (cd == 1 || cd == 3) {
-                        pu = __dadd_rn(pu, A.f_pos[q]);
-                    } else if (cd == 2) {
-                        ou = __dadd_rn(ou, ov[q]);
-                        pu = __dadd_rn(pu, pv[q]);
+            // parents [plo, lo): fold committed children in descending child
+            // rank (the reference's serial same-parent commit order), DK_UF
+            // parents per thread with their child loads issued together
+            const int64_t plo = A.level_off[lv - 1];
+            const int64_t PW = lo - plo;
+            const int64_t ub = plo + (PW * b) / G, ue = plo + (PW * (b + 1)) / G;
+            for (int64_t u0 = ub + tid; u0 < ue; u0 += (int64_t)DK_UF * bd) {
+                int32_t clo[DK_UF], cnt[DK_UF];
+                double pu[DK_UF], ou[DK_UF];
+                int32_t mx = 0;
+#pragma unroll
+                for (int i = 0; i < DK_UF; ++i) {
+                    const int64_t u = u0 + (int64_t)i * bd;
+                    cnt[i] = 0;
+                    if (u < ue) {
+                        clo[i] = A.child_lo[u];
+                        cnt[i] = A.child_cnt[u];
+                        pu[i] = A.p0[u];
+                        ou[i] = A.om0[u];
+                    }
+                    mx = max(mx, cnt[i]);
+                }
+                for (int32_t r = 0; r < mx; ++r) {
+                    int8_t cd[DK_UF];
+                    int32_t ex[DK_UF];
+                    double fq[DK_UF], oq[DK_UF], pq[DK_UF];
+#pragma unroll
+                    for (int i = 0; i < DK_UF; ++i)
+                        if (r < cnt[i]) {
+                            const int64_t q = clo[i] + cnt[i] - 1 - r;
+                            cd[i] = A.code[q];
+                            ex[i] = A.excl[q];
+                            fq[i] = A.f_pos[q];
+                            oq[i] = ov[q];
+                            pq[i] = pv[q];
+                        }
+#pragma unroll
+                    for (int i = 0; i < DK_UF; ++i)
+                        if (r < cnt[i]) {
+                            const int64_t q = clo[i] + cnt[i] - 1 - r;
+                            const uint32_t c = (uint32_t)(hi - 1 - q);
+                            const int64_t e = (int64_t)s_pre[c / CH] + ex[i];
+                            int8_t d = cd[i];
+                            if (e < need) {
+                                if (d == 1) A.spars[j + e] = __ddiv_rn(__dadd_rn(fq[i], pq[i]), oq[i]);
+                            } else {
+                                A.code[q] = 0;
+                                d = 0;
+                            }
+                            if (d == 1 || d == 3) {
+                                pu[i] = __dadd_rn(pu[i], fq[i]);
+                            } else if (d == 2) {
+                                ou[i] = __dadd_rn(ou[i], oq[i]);
+                                pu[i] = __dadd_rn(pu[i], pq[i]);
+                            }
+                        }
+                }
+#pragma unroll
+                for (int i = 0; i < DK_UF; ++i) {
+                    const int64_t u = u0 + (int64_t)i * bd;
+                    if (u < ue) {
+                        A.p[u] = pu[i];
+                        A.om[u] = ou[i];
                     }
                 }
-                A.p[u] = pu;
-                A.om[u] = ou;
+            }
+        } else {
+            // the root level has no parent fold: commit in place
+            for (uint32_t c = cb + tid; c < ce; c += bd) {
+                const int64_t pos = hi - 1 - c;
+                const int64_t e = (int64_t)s_pre[b] + A.excl[pos];
+                if (e < need) {
+                    if (A.code[pos] == 1) A.spars[j + e] = __ddiv_rn(__dadd_rn(A.f_pos[pos], pv[pos]), ov[pos]);
+                } else {
+                    A.code[pos] = 0;
+                }
             }
         }
         j += (tot < need) ? tot : need;
@@ -348,6 +458,7 @@ int decide_grid_size(int64_t max_width) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decide_kernel, 512, 0);
     int64_t want = (max_width + 8191) / 8192;
     int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    if (cap > DK_MAXG) cap = DK_MAXG;
     if (want < 1) want = 1;
     return (int)(want < cap ? want : cap);
 }
