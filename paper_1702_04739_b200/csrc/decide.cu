@@ -57,6 +57,9 @@ constexpr int DK_MAXG = 1024;  // chunk counts live in scratch[0, 1024)
 #ifndef DK_UF
 #define DK_UF 2   // fold: parents per thread per pass
 #endif
+#ifndef DK_FOLD_COND
+#define DK_FOLD_COND 0  // 1: load a child's f / omega / p only where its condition uses them
+#endif
 #ifndef DK_MINB
 #define DK_MINB 2 // resident CTAs per SM the register budget is sized for
 #endif
@@ -217,9 +220,21 @@ __global__ void __launch_bounds__(512, DK_MINB) decide_kernel(DecideArgs A) {
                             const int64_t q = clo[i] + cnt[i] - 1 - r;
                             cd[i] = A.code[q];
                             ex[i] = A.excl[q];
+#if DK_FOLD_COND
+                        }
+#pragma unroll
+                    for (int i = 0; i < DK_UF; ++i)
+                        if (r < cnt[i]) {
+                            const int64_t q = clo[i] + cnt[i] - 1 - r;
+                            // only the values this child's condition uses
+                            fq[i] = cd[i] == 1 || cd[i] == 3 ? A.f_pos[q] : 0.0;
+                            oq[i] = cd[i] == 2 || cd[i] == 1 ? ov[q] : 0.0;
+                            pq[i] = cd[i] == 1 || cd[i] == 2 ? pv[q] : 0.0;
+#else
                             fq[i] = A.f_pos[q];
                             oq[i] = ov[q];
                             pq[i] = pv[q];
+#endif
                         }
 #pragma unroll
                     for (int i = 0; i < DK_UF; ++i)
