@@ -640,61 +640,46 @@ __host__ __device__ __forceinline__ int seg_depth(int64_t m) {
     return T;
 }
 
-// sum over segments of 2 * 2^T: 2^T <= max(1, 2m/64) and the segment
-// lengths total at most 2n (boundary) + n + n (members twice)
-static inline int64_t cost_slot_bound(int64_t n, int64_t k) { return 2 * (4 * n / 32 + 3 * k) + 64; }
 
 // Per (cluster, quantity) segment: 0 = boundary flows, 1 = potentials,
-// 2 = masses.  slot_off holds each segment's scratch offset (2 * 2^T values
-// and flags, double-buffered) computed on the device from the bounds.
+// 2 = masses.  A segment of m values is the numpy pairwise recursion cut at
+// depth T (seg_depth): S = 2^T slots (slot_value), folded pairwise back up.
+// The slots are split into aligned blocks of SEG_B (one CTA each, so a
+// cluster holding most of the tree no longer runs on one CTA); each block
+// folds to the value of its subtree node, and one CTA per segment folds the
+// block values.  Same binary tree, same additions: bitwise the single-CTA
+// fold.
+constexpr int SEG_B = 2048;
+
+// slot blocks over all segments: 2^T <= max(1, 2m/64) slots per segment,
+// segment lengths total at most 2n (boundary) + n + n (members twice), one
+// block per SEG_B slots or per nonempty segment
+static inline int64_t cost_block_bound(int64_t n, int64_t k) { return (4 * n / 32) / SEG_B + 3 * k + 1; }
+
+// seg_blocks: per segment the number of slot blocks (0 for an empty one);
+// blk_off: their exclusive prefix, blk_off[3k] = total.
 __global__ void slot_offsets_kernel(const int64_t* __restrict__ bseg, const int64_t* __restrict__ mseg,
-                                    int64_t k, int64_t* __restrict__ slot_off) {
+                                    int64_t k, int64_t* __restrict__ blk_off) {
     int64_t acc = 0;
     for (int64_t q = 0; q < 3 * k; ++q) {
         const int64_t c = q / 3;
         const int64_t* seg = (q % 3) == 0 ? bseg : mseg;
         const int64_t m = seg[c + 1] - seg[c];
-        slot_off[q] = acc;
-        acc += 2 * (int64_t(1) << seg_depth(m));
+        blk_off[q] = acc;
+        if (m > 0) {
+            const int64_t S = int64_t(1) << seg_depth(m);
+            acc += S > SEG_B ? S / SEG_B : 1;
+        }
     }
-    slot_off[3 * k] = acc;
+    blk_off[3 * k] = acc;
 }
 
-// One CTA per segment: slot values, then a binary fold where an empty right
-// slot passes the left value through unchanged (the leaf above it IS the node).
-__global__ void segment_sum_kernel(const double* __restrict__ bvals_sorted,
-                                   const int32_t* __restrict__ mvals_sorted,
-                                   const double* __restrict__ omega, const double* __restrict__ p,
-                                   const int64_t* __restrict__ bseg, const int64_t* __restrict__ mseg,
-                                   const int64_t* __restrict__ slot_off, double* __restrict__ vals,
-                                   uint8_t* __restrict__ flags, double* __restrict__ sums) {
-    const int64_t c = blockIdx.x / 3;
-    const int what = blockIdx.x % 3;
-    const int64_t* seg = what == 0 ? bseg : mseg;
-    const int64_t a = seg[c], m = seg[c + 1] - seg[c];
-    if (m == 0) {
-        if (threadIdx.x == 0) sums[blockIdx.x] = 0.0;
-        return;
-    }
-    const int T = seg_depth(m);
-    const int64_t S = int64_t(1) << T;
-    double* v0 = vals + slot_off[blockIdx.x];
-    double* v1 = v0 + S;
-    uint8_t* e0 = flags + slot_off[blockIdx.x];
-    uint8_t* e1 = e0 + S;
-    auto get = [&](int64_t i) -> double {
-        if (what == 0) return bvals_sorted[a + i];
-        const int32_t v = mvals_sorted[a + i];
-        return what == 1 ? p[v] : omega[v];
-    };
-    for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {
-        bool e = false;
-        v0[s] = slot_value(get, m, T, s, e);
-        e0[s] = e;
-    }
-    __syncthreads();
-    for (int64_t w = S; w > 1; w >>= 1) {
-        for (int64_t i = threadIdx.x; i < w / 2; i += blockDim.x) {
+// In-shared-memory pairwise fold of w (a power of two) slot values; an
+// empty right child passes the left value through (the leaf above it IS the
+// node); a node is empty iff its left child is.  Returns the root.
+__device__ double fold_slots(double* v0, double* v1, uint8_t* e0, uint8_t* e1, int w, bool& empty) {
+    for (; w > 1; w >>= 1) {
+        for (int i = threadIdx.x; i < w / 2; i += blockDim.x) {
             const double l = v0[2 * i], r = v0[2 * i + 1];
             v1[i] = e0[2 * i + 1] ? l : __dadd_rn(l, r);
             e1[i] = e0[2 * i];
@@ -703,7 +688,90 @@ __global__ void segment_sum_kernel(const double* __restrict__ bvals_sorted,
         double* tv = v0; v0 = v1; v1 = tv;
         uint8_t* te = e0; e0 = e1; e1 = te;
     }
-    if (threadIdx.x == 0) sums[blockIdx.x] = __dadd_rn(0.0, v0[0]);
+    empty = e0[0];
+    const double r = v0[0];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(256) segment_part_kernel(const double* __restrict__ bvals_sorted,
+                                                           const int32_t* __restrict__ mvals_sorted,
+                                                           const double* __restrict__ omega,
+                                                           const double* __restrict__ p,
+                                                           const int64_t* __restrict__ bseg,
+                                                           const int64_t* __restrict__ mseg, int64_t k,
+                                                           const int64_t* __restrict__ blk_off,
+                                                           double* __restrict__ part, uint8_t* __restrict__ pempty) {
+    __shared__ double v[2][SEG_B];
+    __shared__ uint8_t e[2][SEG_B];
+    const int64_t g = blockIdx.x;
+    const int64_t nseg = 3 * k;
+    if (g >= blk_off[nseg]) return;
+    int64_t lo = 0, hi = nseg;   // last q with blk_off[q] <= g (empty segments own no block)
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (blk_off[mid] <= g) lo = mid; else hi = mid;
+    }
+    const int64_t q = lo, c = q / 3;
+    const int what = (int)(q % 3);
+    const int64_t* seg = what == 0 ? bseg : mseg;
+    const int64_t a = seg[c], m = seg[c + 1] - seg[c];
+    const int T = seg_depth(m);
+    const int64_t S = int64_t(1) << T;
+    const int B = S > SEG_B ? SEG_B : (int)S;
+    const int64_t s0 = (g - blk_off[q]) * B;
+    auto get = [&](int64_t i) -> double {
+        if (what == 0) return bvals_sorted[a + i];
+        const int32_t x = mvals_sorted[a + i];
+        return what == 1 ? p[x] : omega[x];
+    };
+    for (int s = threadIdx.x; s < B; s += blockDim.x) {
+        bool em = false;
+        v[0][s] = slot_value(get, m, T, s0 + s, em);
+        e[0][s] = em;
+    }
+    __syncthreads();
+    bool em;
+    const double r = fold_slots(v[0], v[1], e[0], e[1], B, em);
+    if (threadIdx.x == 0) {
+        part[g] = r;
+        pempty[g] = em;
+    }
+}
+
+__global__ void __launch_bounds__(256) segment_sum_kernel(const int64_t* __restrict__ blk_off,
+                                                          const double* __restrict__ part,
+                                                          const uint8_t* __restrict__ pempty,
+                                                          double* __restrict__ sums) {
+    __shared__ double v[2][SEG_B];
+    __shared__ uint8_t e[2][SEG_B];
+    __shared__ double cv[2][64];
+    __shared__ uint8_t ce[2][64];
+    const int64_t q = blockIdx.x;
+    const int64_t b0 = blk_off[q], nb = blk_off[q + 1] - b0;   // a power of two (or 0)
+    if (nb == 0) {
+        if (threadIdx.x == 0) sums[q] = 0.0;
+        return;
+    }
+    const int C = nb > SEG_B ? SEG_B : (int)nb;
+    const int chunks = (int)(nb / C);   // <= 64 for n < 2^32 (m < 2^33, S <= 2^28)
+    for (int ch = 0; ch < chunks; ++ch) {
+        for (int s = threadIdx.x; s < C; s += blockDim.x) {
+            v[0][s] = part[b0 + (int64_t)ch * C + s];
+            e[0][s] = pempty[b0 + (int64_t)ch * C + s];
+        }
+        __syncthreads();
+        bool em;
+        const double r = fold_slots(v[0], v[1], e[0], e[1], C, em);
+        if (threadIdx.x == 0) {
+            cv[0][ch] = r;
+            ce[0][ch] = em;
+        }
+    }
+    __syncthreads();
+    bool em;
+    const double r = fold_slots(cv[0], cv[1], ce[0], ce[1], chunks, em);
+    if (threadIdx.x == 0) sums[q] = __dadd_rn(0.0, r);
 }
 
 __global__ void miso_kernel(const double* __restrict__ sums, int64_t k, double* __restrict__ out) {
@@ -731,10 +799,10 @@ cudaError_t launch_cost(const int32_t* lab32, const int32_t* parent_v, const dou
     double* bvals_s = (double*)take(16 * n);
     int64_t* mseg = (int64_t*)take(8 * (k + 2));
     int64_t* bseg = (int64_t*)take(8 * (k + 2));
-    int64_t* slot_off = (int64_t*)take(8 * (3 * k + 1));
-    const int64_t slots = cost_slot_bound(n, k);
-    double* svals = (double*)take(8 * slots);
-    uint8_t* sflags = (uint8_t*)take(slots);
+    int64_t* blk_off = (int64_t*)take(8 * (3 * k + 1));
+    const int64_t nblk = cost_block_bound(n, k);
+    double* part = (double*)take(8 * nblk);
+    uint8_t* pempty = (uint8_t*)take(nblk);
     if ((size_t)(w - reinterpret_cast<char*>(work)) > work_bytes) return cudaErrorInvalidValue;
 
     cost_keys_kernel<<<nb(n, 256), 256, 0, st>>>(lab32, parent_v, flow, omega, p, n, k, mkeys, mvals,
@@ -753,20 +821,21 @@ cudaError_t launch_cost(const int32_t* lab32, const int32_t* parent_v, const dou
     cudaFreeAsync(tmp, st);
     segment_bounds_kernel<<<nb(k + 1, 128), 128, 0, st>>>(mkeys_s, n, k, mseg);
     segment_bounds_kernel<<<nb(k + 1, 128), 128, 0, st>>>(bkeys_s, 2 * n, k, bseg);
-    slot_offsets_kernel<<<1, 1, 0, st>>>(bseg, mseg, k, slot_off);
-    segment_sum_kernel<<<(unsigned)(3 * k), 256, 0, st>>>(bvals_s, mvals_s, omega, p, bseg, mseg,
-                                                          slot_off, svals, sflags, sums);
+    slot_offsets_kernel<<<1, 1, 0, st>>>(bseg, mseg, k, blk_off);
+    segment_part_kernel<<<(unsigned)nblk, 256, 0, st>>>(bvals_s, mvals_s, omega, p, bseg, mseg, k, blk_off,
+                                                        part, pempty);
+    segment_sum_kernel<<<(unsigned)(3 * k), 256, 0, st>>>(blk_off, part, pempty, sums);
     miso_kernel<<<1, 1, 0, st>>>(sums, k, miso);
-    note_launch(6);
+    note_launch(7);
     return cudaGetLastError();
 }
 
 size_t cost_work_bytes(int64_t n, int64_t k) {
-    const int64_t slots = cost_slot_bound(n, k);
+    const int64_t nblk = cost_block_bound(n, k);
     size_t b = 0;
     auto add = [&](size_t bytes) { b += (bytes + 255) & ~size_t(255); };
     add(8 * n); add(8 * n); add(4 * n); add(4 * n); add(16 * n); add(16 * n); add(16 * n); add(16 * n);
-    add(8 * (k + 2)); add(8 * (k + 2)); add(8 * (3 * k + 1)); add(8 * slots); add(slots);
+    add(8 * (k + 2)); add(8 * (k + 2)); add(8 * (3 * k + 1)); add(8 * nblk); add(nblk);
     return b;
 }
 
