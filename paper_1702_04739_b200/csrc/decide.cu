@@ -324,6 +324,9 @@ __global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
     const int K = A.K;
     const int Gi = gridDim.x / K;
     const int kk = blockIdx.x / Gi, bi = blockIdx.x % Gi;
+    // one CTA per instance: the instances are independent, so CTA barriers
+    // replace the grid barriers and each CTA stops at its own k-th cut
+    const bool solo = Gi == 1;
     const int64_t n = A.n;
     const double thr = A.thr[kk];
     double* om = A.om + kk * n;
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
             }
         }
         if (tid == 0) chunk_cnt[bi] = (int32_t)carry;
-        grid_barrier(A.bar);
+        if (solo) __syncthreads(); else grid_barrier(A.bar);
         if (tid == 0) {
             int64_t pre = 0, tot = 0;
             for (int q = 0; q < Gi; ++q) {
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
                 const int64_t pos = hi - 1 - c;
                 if (off + excl[pos] >= need) code[pos] = 0;
             }
-        grid_barrier(A.bar);
+        if (solo) __syncthreads(); else grid_barrier(A.bar);
         if (lv > 0 && active) {
             const int64_t plo = A.level_off[lv - 1], phi = lo;
             const int64_t PW = phi - plo;
@@ -424,6 +427,11 @@ __global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
         }
         if (active) j += (tot < need) ? tot : need;
         // instances publish whether they are done; stop when all are
+        if (solo) {
+            __syncthreads();
+            if (j >= A.k) break;
+            continue;
+        }
         if (bi == 0 && tid == 0) A.j_out[kk] = j;
         grid_barrier(A.bar);
         if (tid == 0) {
