@@ -466,6 +466,19 @@ def main():
                                 "pairs; the symmetric kernel computes each unordered pair once "
                                 "(plus a 128-column leaf strip), so 'executed' is the FP64 pipe's view")
 
+    if roofline is None and dom == "decide":
+        # tiny inputs (C1): the tree phase dominates; HBM roofline of the
+        # decision sweeps with the sequential-equivalent algorithmic bytes
+        # (45 B per vertex per bisection step)
+        steps_walked = max(1, int(run.result.iterations))
+        achieved = 45.0 * n * steps_walked / (kernels["decide"]["ms_total"] * 1e-3) / 1e9
+        peak = float(peaks().get("hbm_gbs") or 7700.0)
+        roofline = {"kernel": "decide", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "note": "level-synchronous sweeps over a narrow MST tree (hundreds of levels of a few "
+                            "vertices): latency-bound, not bandwidth-bound; algorithmic bytes = 45 B x n per "
+                            "bisection step walked"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
