@@ -364,9 +364,12 @@ par_decide = decide
 
 
 def _speculation_depth(dt: DeviceTree) -> int:
-    """Bisection steps per batched sweep: 4 (15 thresholds) on latency-bound
-    trees whose levels are narrow (MST trees of C1-C4), 1 (plain sequential
-    sweeps) on wide, HBM-bound trees (C5).  ISOC_SPEC_M overrides."""
+    """Bisection steps per batched sweep: 4 (15 thresholds, one CTA group
+    each) on latency-bound trees whose levels are narrow (MST trees of
+    C1-C4), 1 (plain sequential sweeps, which stop at their own k-th cut) on
+    wide trees (C5): there a 3-threshold sweep -- split CTAs or shared
+    (decide_multi_kernel) -- costs 2.3x a single one.  ISOC_SPEC_M
+    overrides."""
     env = os.environ.get("ISOC_SPEC_M")
     if env is not None:
         return max(1, min(4, int(env)))
