@@ -97,3 +97,13 @@ def test_pairwise_sum_matches_numpy(oracle_mod):
     for n in (0, 1, 7, 8, 9, 127, 128, 129, 1000, 8193, 123457):
         a = rng.random(n) * 100
         assert oracle_mod.pairwise_sum(a) == float(np.sum(a))
+
+
+def test_oracle_all_flows_underflow_raises_zero_division(oracle_mod):
+    # with sigma so small that every exp(-d/sigma) underflows,
+    # the reference's bracket (phi_min + p_min) / omega_sum raises Python's
+    # ZeroDivisionError (isoperim.py:238-239; checked by running the reference
+    # on this instance: run_pipeline(generate_random(300, 5, 3, 0), 3, sigma=1e-3))
+    pts, _ = oracle_mod.generate_random(300, 5, 3, 0)
+    with pytest.raises(ZeroDivisionError):
+        oracle_mod.run_pipeline(pts, 3, sigma=1e-3)

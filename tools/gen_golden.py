@@ -30,13 +30,19 @@ PIPELINE_CASES = [
     ("d3_n50", 50, 3, 4, 7, 0.0, 0, "auto"),
     ("d2_n777_sigma2", 777, 2, 5, 11, 0.0, 3, 2.0),
     ("d13_n178", 178, 13, 3, 5, 0.0, 0, "auto"),
+    # explicit small sigma: most flows exp(-d/sigma) underflow to subnormals / 0
+    ("d5_n300_sigma0.02", 300, 5, 3, 0, 0.0, 0, 0.02),
+    ("d5_n300_sigma0.05", 300, 5, 3, 0, 0.0, 0, 0.05),
 ]
 
 
 def main() -> None:
     if os.environ.get("NPY_DISABLE_CPU_FEATURES") != PIN:
         env = dict(os.environ, NPY_DISABLE_CPU_FEATURES=PIN)
-        sys.exit(subprocess.call([sys.executable, __file__], env=env))
+        sys.exit(subprocess.call([sys.executable, __file__, *sys.argv[1:]], env=env))
+    only = None
+    if len(sys.argv) > 2 and sys.argv[1] == "--only":
+        only = set(sys.argv[2].split(","))
     sys.path.insert(0, "/root/reference/pkg/src")
     sys.path.insert(0, "/root/reference/pkg/tests")
     import numpy as np
@@ -45,6 +51,8 @@ def main() -> None:
 
     OUT.mkdir(parents=True, exist_ok=True)
     for name, n, d, k, seed, alpha, root, sigma in PIPELINE_CASES:
+        if only is not None and name not in only:
+            continue
         pts, _ = ic.generate_random(n, d, k, seed)
         run = ic.run_pipeline(pts, k, sigma=sigma, alpha=alpha, root=root, engine="seq")
         dist = ic.distance_matrix(pts, workers=1)
@@ -72,6 +80,8 @@ def main() -> None:
             row0=dist[0].copy(), rowlast=dist[n - 1].copy(),
         )
         print(name, "sigma", run.sigma, "miso", r.miso, "iters", r.iterations, file=sys.stderr)
+    if only is not None:
+        return
 
     # tree-phase instances from the reference's own random_instance
     rng = np.random.Generator(np.random.PCG64(20260814))
