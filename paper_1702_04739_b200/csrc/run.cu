@@ -177,6 +177,11 @@ int run_impl(const double* points, int64_t n, int32_t d, int64_t k, double sigma
     RCK(alloc(v, (size_t)(n - 1) * 4, st));
     RCK(alloc(w, (size_t)(n - 1) * 8, st));
     RCK(isoc_mst_edges(h, u.get<int32_t>(), v.get<int32_t>(), w.get<double>()));
+    // prim_mst's tie rule: an exact tie at a component minimum -> replay Prim
+    // exactly (isoc_prim_edges); ISOC_MST=prim forces it (pipeline._tie_rule)
+    const char* mst_env = std::getenv("ISOC_MST");
+    if (ties > 0 || (mst_env && std::strcmp(mst_env, "prim") == 0))
+        RCK(isoc_prim_edges(X, n, d, root, u.get<int32_t>(), v.get<int32_t>(), w.get<double>(), st));
     isoc_tree* tree = nullptr;
     RCK(isoc_tree_from_edges(u.get<int32_t>(), v.get<int32_t>(), w.get<double>(), n, root, sig, st, &tree));
     struct TreeGuard {

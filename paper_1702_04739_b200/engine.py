@@ -319,6 +319,15 @@ class CudaBackend:
         check(self.lib.isoc_mst_edges(h, _ptr(u), _ptr(v), _ptr(w)))
         return u, v, w
 
+    def prim_edges(self, X, n: int, d: int, root: int):
+        """isoc_prim_edges: the reference's Prim tree (tie rule included)."""
+        torch = self.torch
+        u = self.empty((n - 1,), torch.int32)
+        v = self.empty((n - 1,), torch.int32)
+        w = self.empty((n - 1,), torch.float64)
+        check(self.lib.isoc_prim_edges(_ptr(X), n, d, root, _ptr(u), _ptr(v), _ptr(w), self.stream))
+        return u, v, w
+
     def mst_destroy(self, h) -> None:
         self.lib.isoc_mst_destroy(h)
 

@@ -242,11 +242,23 @@ def _boruvka(P: _Points, nn=None, sigma: Optional[float] = None) -> tuple:
                           device=getattr(b, "device", "cpu"))
         comm.allreduce_sum_(tt)
         stats["exact_ties"], stats["exact_rescans"] = (int(x) for x in tt.tolist())
-    if stats["exact_ties"]:
-        warnings.warn(
-            f"{stats['exact_ties']} exact distance ties at a component minimum: the MST may differ "
-            "from the reference's Prim tie rule (SURVEY 8c, Appendix A.6)", RuntimeWarning, stacklevel=3)
     return u, v, w, omega_loc, stats
+
+
+def _tie_rule(P: _Points, u, v, w, stats: dict, root: int):
+    """prim_mst's tie rule (mst.py:144-166, _primitives.py:69-92).
+
+    The lexicographic Boruvka MST is the reference's Prim tree whenever every
+    component minimum is unique.  When a round saw an
+    exact distance tie (the count is global after the all-reduce, so every
+    rank decides alike), Prim is replayed exactly on the device from `root`
+    (isoc_prim_edges; X is replicated on every rank).  ISOC_MST=prim forces it.
+    """
+    stats["prim_replay"] = 0
+    if stats["exact_ties"] or os.environ.get("ISOC_MST", "") == "prim":
+        stats["prim_replay"] = 1
+        return P.b.prim_edges(P.X, P.n, P.d, root)
+    return u, v, w
 
 
 def _progress(c: int, comps: int, stats: dict) -> int:
@@ -292,7 +304,8 @@ def minimum_spanning_tree(points, sigma: float, root: int = 0) -> RootedTree:
     P = _Points(points)
     if not (0 <= root < P.n):
         raise ValueError(f"root must be in [0, {P.n}), got {root}")
-    u, v, w, _, _ = _boruvka(P)
+    u, v, w, _, stats = _boruvka(P)
+    u, v, w = _tie_rule(P, u, v, w, stats, root)
     dt = P.b.tree_from_edges(u, v, w, P.n, root, sigma)
     return _rooted_tree_view(dt, root)
 
@@ -558,6 +571,7 @@ def run_pipeline(
     # round 2); its time is booked under "affinity" like the reference's
     # node_weights
     u, v, w, om_loc, stats = _boruvka(P, nn, sigma=sigma_val)
+    u, v, w = _tie_rule(P, u, v, w, stats, root)
     dt = b.tree_from_edges(u, v, w, n, root, sigma_val)
     torch.cuda.synchronize()
     mst_ms = (time.perf_counter() - t0) * 1e3 - stats["omega_ms"]
