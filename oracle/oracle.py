@@ -73,6 +73,14 @@ def lib():
         L.oc_subpartition_cost.argtypes = [P, I64, P, P, P, P]
         L.oc_num_threads.restype = ctypes.c_int
         L.oc_set_threads.argtypes = [ctypes.c_int]
+        I = ctypes.c_int
+        L.ocf_isa.restype = I
+        L.ocf_flat_distance_sum.restype = D
+        L.ocf_flat_distance_sum.argtypes = [P, I64, I]
+        L.ocf_omega_knn.restype = I
+        L.ocf_omega_knn.argtypes = [P, I64, I, D, I64, I64, I, P, P, P]
+        L.ocf_rescan_rows.restype = I
+        L.ocf_rescan_rows.argtypes = [P, I64, I, P, I64, P, I, P, P]
         _lib = L
     return _lib
 
@@ -376,3 +384,207 @@ def solve_tree(parent, flows, omega, p, k: int) -> tuple[Result, Tree, Extrema]:
     tree = tree_from_parent_list(parent, flows)
     ext = extrema(tree, omega, p)
     return run_bisection(tree, omega, p, ext, k), tree, ext
+
+
+# ------------------------------------------------ full-size oracle (C3/C4)
+# isoc_fast.c kernels (same per-pair operation order, vectorised across
+# pairs) + a certified Boruvka for Prim's edge set.  Used to produce the
+# full-size parity fixtures (tools/oracle_full.py) and pinned against the
+# reference at n = 16,000 / 32,000 / 46,340 (tests/test_oracle.py).
+
+class TieError(RuntimeError):
+    """A Boruvka component minimum was attained twice: the MST may not be
+    unique, so the certified path cannot stand in for Prim (use prim_mst)."""
+
+
+def flat_distance_sum_fast(X: np.ndarray) -> float:
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    out = lib().ocf_flat_distance_sum(_p(X), X.shape[0], X.shape[1])
+    if math.isnan(out):
+        raise MemoryError("ocf_flat_distance_sum: allocation failed")
+    return out
+
+
+def auto_sigma_fast(X: np.ndarray) -> float:
+    n = X.shape[0]
+    mean = flat_distance_sum_fast(X) / (n * (n - 1))
+    if not (mean > 0):
+        raise ValueError("all points coincide; no usable distance scale")
+    return mean
+
+
+def omega_knn(X: np.ndarray, sigma: float, K: int = 32):
+    """omega (vertex_weights, affinity.py:175-201; alpha = 0 so p = 0) and each
+    row's K lexicographically smallest (d, j), j != i."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    n, d = X.shape
+    omega = np.empty(n)
+    kd = np.empty((n, K))
+    kj = np.empty((n, K), np.int64)
+    rc = lib().ocf_omega_knn(_p(X), n, d, float(sigma), 0, n, K, _p(omega), _p(kd), _p(kj))
+    if rc:
+        raise MemoryError("ocf_omega_knn: allocation failed")
+    return omega, kd, kj
+
+
+def mst_certified(X: np.ndarray, kd: np.ndarray, kj: np.ndarray, stats: Optional[dict] = None):
+    """Prim's MST edge set (mst.py:128-181) via Boruvka with a uniqueness
+    certificate: every round, every component's minimum outgoing edge is
+    found exactly and must be the ONLY outgoing edge of that weight (else
+    TieError).  A strictly lightest cut edge is in every MST, so the n-1
+    certified edges are the unique MST = Prim's tree.  kd/kj (n x K, sorted
+    by (d, j)) are refined in place by exact rescans of rows whose list
+    cannot decide their component's minimum.  Returns (u, v, w) arrays."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    n, d = X.shape
+    K = kd.shape[1]
+    rows = np.arange(n)
+    comp = np.arange(n, dtype=np.int32)
+    eu = np.empty(0, np.int64)
+    ev = np.empty(0, np.int64)
+    ew = np.empty(0, np.float64)
+    st = stats if stats is not None else {}
+    st.update(rounds=0, rescans=0, rescans_per_round=[], components_per_round=[])
+    ncomp = n
+    while ncomp > 1:
+        st["rounds"] += 1
+        st["components_per_round"].append(int(ncomp))
+        rescanned_this_round = 0
+        for attempt in range(2):
+            valid = kj >= 0
+            ext = valid & (comp[np.where(valid, kj, 0)] != comp[:, None])
+            has = ext.any(1)
+            first = np.argmax(ext, 1)
+            cand_d = np.where(has, kd[rows, first], np.inf)
+            cand_j = np.where(has, kj[rows, first], -1)
+            full = valid[:, K - 1]
+            lb = np.where(full, kd[:, K - 1], np.inf)  # every unlisted j has d >= lb
+            mult = (ext & (kd == cand_d[:, None])).sum(1)
+            unsure = has & full & (kd[:, K - 1] == cand_d)  # unlisted j may tie the row min
+            m = np.full(n, np.inf)
+            np.minimum.at(m, comp, cand_d)
+            mc = m[comp]
+            need = (~has & (lb <= mc)) | (unsure & (cand_d <= mc))
+            if not need.any():
+                break
+            if attempt == 1:
+                raise TieError("more than K exact ties at a row minimum")
+            idx = np.flatnonzero(need).astype(np.int64)
+            nd = np.empty((idx.size, K))
+            nj = np.empty((idx.size, K), np.int64)
+            rc = lib().ocf_rescan_rows(_p(X), n, d, _p(idx), idx.size, _p(comp), K, _p(nd), _p(nj))
+            if rc:
+                raise MemoryError("ocf_rescan_rows: allocation failed")
+            kd[idx] = nd
+            kj[idx] = nj
+            rescanned_this_round += idx.size
+        st["rescans"] += rescanned_this_round
+        st["rescans_per_round"].append(int(rescanned_this_round))
+        # component minima: the attaining rows and their multiplicity
+        at_min = has & (cand_d == mc)
+        cnt = np.bincount(comp[at_min], weights=mult[at_min], minlength=n)
+        if (cnt[comp[at_min]] > 1).any():
+            raise TieError(f"exact tie at a component minimum in Boruvka round {st['rounds']}")
+        a = rows[at_min]
+        b = cand_j[at_min]
+        w = cand_d[at_min]
+        key = np.minimum(a, b) * n + np.maximum(a, b)
+        key, first_idx = np.unique(key, return_index=True)
+        eu = np.concatenate([eu, a[first_idx]])
+        ev = np.concatenate([ev, b[first_idx]])
+        ew = np.concatenate([ew, w[first_idx]])
+        g = coo_matrix((np.ones(eu.size), (eu, ev)), shape=(n, n))
+        ncomp, lab = connected_components(g, directed=False)
+        comp = lab.astype(np.int32)
+    if eu.size != n - 1:
+        raise RuntimeError(f"certified Boruvka produced {eu.size} edges for n={n}")
+    return eu, ev, ew
+
+
+def root_tree(n: int, eu, ev, ew, root: int, sigma: float) -> Tree:
+    """Root the MST edge set like prim_mst does (mst.py:128-181, 46-65):
+    parent by BFS from root; child_id = rank of (d(p,u), u) among p's
+    children (Prim's insertion order); bfs_order reversed."""
+    a = np.concatenate([eu, ev]).astype(np.int64)
+    b = np.concatenate([ev, eu]).astype(np.int64)
+    w = np.concatenate([ew, ew])
+    order = np.lexsort((b, w, a))
+    a, b, w = a[order], b[order], w[order]
+    start = np.searchsorted(a, np.arange(n + 1))
+    parent = np.full(n, NO_VERTEX, np.int64)
+    pdist = np.zeros(n)
+    depth = np.zeros(n, np.int64)
+    child_id = np.zeros(n, np.int64)
+    seen = np.zeros(n, bool)
+    seen[root] = True
+    level = np.array([root], np.int64)
+    out = [level]
+    dep = 0
+    while level.size:
+        s, c = start[level], start[level + 1] - start[level]
+        tot = int(c.sum())
+        if tot == 0:
+            break
+        idx = np.arange(tot) - np.repeat(np.cumsum(c) - c, c) + np.repeat(s, c)
+        src = np.repeat(level, c)
+        dst = b[idx]
+        keep = ~seen[dst]
+        src, dst, wd = src[keep], dst[keep], w[idx][keep]
+        dep += 1
+        seen[dst] = True
+        parent[dst] = src
+        pdist[dst] = wd
+        depth[dst] = dep
+        # rank among siblings: dst is grouped by src (level order) and sorted by (w, b)
+        grp_start = np.r_[0, np.flatnonzero(src[1:] != src[:-1]) + 1]
+        pos = np.arange(dst.size)
+        child_id[dst] = pos - np.repeat(grp_start, np.diff(np.r_[grp_start, dst.size]))
+        level = dst
+        out.append(level)
+    root_first = np.concatenate(out)
+    if root_first.size != n:
+        raise ValueError("edge set does not span the points")
+    flow = np.zeros(n)
+    nonroot = parent != NO_VERTEX
+    flow[nonroot] = exp((-pdist[nonroot]) / sigma)
+    return Tree(parent, flow, depth, child_id, root_first[::-1].copy(), root, int(depth.max()), pdist)
+
+
+@dataclass
+class FullRun:
+    out: PipelineOut
+    total_distance: float
+    mst_stats: dict
+    seconds: dict
+
+
+def run_pipeline_full(points, k: int, sigma="auto", root: int = 0, K: int = 32) -> FullRun:
+    """run_pipeline (pipeline.py:41-104, alpha = 0) at full size: the same
+    numbers as run_pipeline() above, with the n^2 passes vectorised and the
+    MST edge set from the certified Boruvka (raises TieError when the MST
+    is not provably unique)."""
+    import time
+
+    X = np.ascontiguousarray(points, dtype=np.float64)
+    n = X.shape[0]
+    sec = {}
+    t0 = time.perf_counter()
+    sig = auto_sigma_fast(X) if sigma == "auto" else float(sigma)
+    sec["sigma"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    omega, kd, kj = omega_knn(X, sig, K)
+    sec["omega_knn"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    st = {}
+    eu, ev, ew = mst_certified(X, kd, kj, st)
+    tree = root_tree(n, eu, ev, ew, root, sig)
+    sec["mst"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    p = np.zeros(n)
+    ext = extrema(tree, omega, p)
+    res = run_bisection(tree, omega, p, ext, k)
+    sec["partition"] = time.perf_counter() - t0
+    return FullRun(PipelineOut(res, tree, omega, p, sig, ext), math.fsum(ew), st, sec)

@@ -95,8 +95,31 @@ __host__ __device__ __forceinline__ int64_t ps_slot(int64_t b, int64_t i, int64_
     return (r * nbs + b) * rows_pad + (i - n * r / G);
 }
 
-__device__ __forceinline__ bool lex_less(double a, int32_t ja, double b, int32_t jb) {
-    return a < b || (a == b && ja < jb);
+// Round-2 minima carry an exact-tie flag in the sign bit of the column
+// index: (m, jt) with jt = j | TIEBIT when the minimum value m was attained
+// by two different columns (each (row, column) pair is evaluated exactly once
+// over the pass, so two equal candidates are two edges).  Boruvka's
+// comp_tie_kernel turns the flag into an exact_ties count, which makes the
+// pipeline replay Prim's tie rule (mst.py:153-166, _primitives.py:69-92).
+constexpr int32_t TIEBIT = (int32_t)0x80000000u;
+__device__ __forceinline__ int32_t jof(int32_t jt) { return jt & 0x7fffffff; }
+
+__device__ __forceinline__ void tie_merge(double& m, int32_t& mjt, double x, int32_t xjt) {
+    if (x < m) {
+        m = x;
+        mjt = xjt;
+    } else if (x == m && x < INFINITY) {
+        mjt = min(jof(mjt), jof(xjt)) | TIEBIT;
+    }
+}
+// the same on the distance bit patterns (d >= 0 orders like its bits)
+__device__ __forceinline__ void tie_merge_bits(uint64_t& m, int32_t& mjt, uint64_t x, int32_t xjt) {
+    if (x < m) {
+        m = x;
+        mjt = xjt;
+    } else if (x == m && x < 0x7ff0000000000000ull) {
+        mjt = min(jof(mjt), jof(xjt)) | TIEBIT;
+    }
 }
 
 __device__ __forceinline__ double csum_push(double* slots, int idx, double v) {
@@ -264,20 +287,20 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                     for (int j = 0; j < 8; ++j) {
                         const bool ok = (!CHK || (i < rlim && LCOL(j) < clim)) && ts.comp_c[LCOL(j)] != cr;
                         const uint64_t bv = (uint64_t)__double_as_longlong(acc[i][j]);
-                        if (ok && bv < m) { m = bv; mj = (int32_t)(gcb + LCOL(j)); }
+                        if (ok) tie_merge_bits(m, mj, bv, (int32_t)(gcb + LCOL(j)));
                     }
 #pragma unroll
                     for (int off = 1; off < 8; off <<= 1) {
                         const uint64_t om = (uint64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off);
                         const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
-                        if (om < m || (om == m && oj < mj)) { m = om; mj = oj; }
+                        tie_merge_bits(m, mj, om, oj);
                     }
                     if (cl == 0) {
                         const int r = rg * 4 + i;
                         const double md = __longlong_as_double((long long)m);
                         double pm = tj == 0 ? INFINITY : ts.rmin[r];
                         int32_t pj = tj == 0 ? INT32_MAX : ts.rminj[r];
-                        if (lex_less(md, mj, pm, pj)) { pm = md; pj = mj; }
+                        tie_merge(pm, pj, md, mj);
                         ts.rmin[r] = pm;
                         ts.rminj[r] = pj;
                     }
@@ -293,13 +316,13 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                         for (int i = 0; i < 4; ++i) {
                             const bool ok = (!CHK || (i < rlim && LCOL(j) < clim)) && ts.comp_r[rg * 4 + i] != cc;
                             const uint64_t bv = (uint64_t)__double_as_longlong(acc[i][j]);
-                            if (ok && bv < m) { m = bv; mj = (int32_t)(gr0 + i); }
+                            if (ok) tie_merge_bits(m, mj, bv, (int32_t)(gr0 + i));
                         }
 #pragma unroll
                         for (int off = 8; off < 32; off <<= 1) {
                             const uint64_t om = (uint64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off);
                             const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
-                            if (om < m || (om == m && oj < mj)) { m = om; mj = oj; }
+                            tie_merge_bits(m, mj, om, oj);
                         }
                         if ((lane >> 3) == 0) {
                             ts.xcm[w][LCOL(j)] = __longlong_as_double((long long)m);
@@ -377,7 +400,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                             if (want_min) {
                                 double m = sm.rowm[r];
                                 int32_t mj = sm.rowj[r];
-                                if (lex_less(ts.rmin[r], ts.rminj[r], m, mj)) { m = ts.rmin[r]; mj = ts.rminj[r]; }
+                                tie_merge(m, mj, ts.rmin[r], ts.rminj[r]);
                                 PSm[o] = m;
                                 PSj[o] = mj;
                             }
@@ -409,8 +432,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 if (want_min) {
                     double m = ts.cmin[col];
                     int32_t mj = ts.cminj[col];
-                    for (int h = 0; h < 8; ++h)
-                        if (lex_less(ts.xcm[h][c], ts.xcj[h][c], m, mj)) { m = ts.xcm[h][c]; mj = ts.xcj[h][c]; }
+                    for (int h = 0; h < 8; ++h) tie_merge(m, mj, ts.xcm[h][c], ts.xcj[h][c]);
                     ts.cmin[col] = m;
                     ts.cminj[col] = mj;
                 }
@@ -434,7 +456,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
 }
 
 // omega[i] = pow2 fold of PS[0..nbs)[i] (complete 1024-wide subtrees, zero
-// padded); round-2 minimum over the blocks (ties -> smaller column).  With G
+// padded); round-2 minimum over the blocks (ties -> smaller column, flagged).  With G
 // senders (the sharded pass after its all-to-all) slot (g, b, r) sits at
 // (g * nbs + b) * stride + r and exactly one sender produced each (b, r);
 // the others hold 0 / (inf, INT32_MAX), so the sum over g is exact.
@@ -461,9 +483,7 @@ __global__ void omega_finish_kernel(const double* __restrict__ PS, const double*
         if (PSm) {
             for (int g = 0; g < G; ++g) {
                 const int64_t o = ((int64_t)g * nbs + b) * stride + i;
-                const double x = PSm[o];
-                const int32_t xj = PSj[o];
-                if (lex_less(x, xj, m, mj)) { m = x; mj = xj; }
+                tie_merge(m, mj, PSm[o], PSj[o]);
             }
         }
     }
@@ -476,9 +496,9 @@ __global__ void omega_finish_kernel(const double* __restrict__ PS, const double*
         }
     omega[i] = acc;
     if (PSm) {
-        nn_j[i] = mj == INT32_MAX ? -1 : mj;
+        nn_j[i] = jof(mj) == INT32_MAX ? -1 : jof(mj);
         nn_d[i] = m;
-        nn_tie[i] = 0;
+        nn_tie[i] = (int8_t)((mj & TIEBIT) != 0);
     }
 }
 

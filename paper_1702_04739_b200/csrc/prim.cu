@@ -46,6 +46,17 @@ __device__ __forceinline__ void warp_min(double& v, int64_t& i) {
     }
 }
 
+// DENSE: X is the (n, n) distance matrix (the dense stage API, prim_mst(dist));
+// row u is read coalesced as D[u*n + j].  Otherwise X is (n, d) points and the
+// distance is recomputed exactly in scipy order.
+template <bool DENSE>
+__device__ __forceinline__ double prim_dist(const double* __restrict__ X, int64_t n, int d, int64_t u,
+                                            int64_t j) {
+    if (DENSE) return X[u * n + j];
+    return exact_dist(X + u * d, X + j * d, d);
+}
+
+template <bool DENSE>
 __global__ void __launch_bounds__(PRIM_THREADS) prim_kernel(
     const double* __restrict__ X, int64_t n, int d, int64_t root, double* key, int32_t* from,
     uint8_t* done, double* pv, int64_t* pi, int32_t* eu, int32_t* ev, double* ew, unsigned int* bar) {
@@ -60,13 +71,12 @@ __global__ void __launch_bounds__(PRIM_THREADS) prim_kernel(
     for (int64_t step = 0; step < n - 1; ++step) {
         double bv = 0.0;
         int64_t bi = -1;
-        const double* xu = X + u * d;
         for (int64_t j = tid; j < n; j += stride) {
             if (step == 0) {
                 // best = d[root], best_from = root (mst.py:144-147)
                 done[j] = (j == root);
                 from[j] = (int32_t)root;
-                key[j] = exact_dist(X + root * d, X + j * d, d);
+                key[j] = prim_dist<DENSE>(X, n, d, root, j);
                 if (j == root) continue;
             } else {
                 if (done[j]) continue;
@@ -74,7 +84,7 @@ __global__ void __launch_bounds__(PRIM_THREADS) prim_kernel(
                     done[j] = 1;
                     continue;
                 }
-                const double r = exact_dist(xu, X + j * d, d);
+                const double r = prim_dist<DENSE>(X, n, d, u, j);
                 if (r < key[j]) {       // strict: ties keep the earlier attach vertex
                     key[j] = r;
                     from[j] = (int32_t)u;
@@ -122,18 +132,19 @@ __global__ void __launch_bounds__(PRIM_THREADS) prim_kernel(
 
 }  // namespace
 
-extern "C" int isoc_prim_edges(const double* X, int64_t n, int32_t d, int64_t root, int32_t* u,
-                               int32_t* v, double* w, void* stream) {
+static int prim_launch(bool dense, const double* X, int64_t n, int32_t d, int64_t root, int32_t* u,
+                       int32_t* v, double* w, void* stream) {
     if (n < 2) return isoc::set_error(ISOC_EINVAL, "need at least 2 vertices");
     if (n > INT32_MAX) return isoc::set_error(ISOC_EINVAL, "n too large for int32 edge ids");
     if (root < 0 || root >= n)
         return isoc::set_error(ISOC_EINVAL, "root must be in [0, %lld), got %lld", (long long)n,
                                (long long)root);
     cudaStream_t st = (cudaStream_t)stream;
+    const void* kern = dense ? (const void*)prim_kernel<true> : (const void*)prim_kernel<false>;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prim_kernel, PRIM_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PRIM_THREADS, 0);
     if (per_sm < 1) return isoc::set_error(ISOC_ECUDA, "prim_kernel cannot be resident");
     int G = sms;  // one CTA per SM: the step is barrier-latency bound
     const int64_t need = (G + 31) / 32 * 32;
@@ -155,11 +166,21 @@ extern "C" int isoc_prim_edges(const double* X, int64_t n, int32_t d, int64_t ro
     cudaMemsetAsync(bar, 0, 64, st);
     int dd = d;
     void* args[] = {(void*)&X, &n, &dd, &root, &key, &from, &done, &pv, &pi, &u, &v, &w, &bar};
-    e = cudaLaunchCooperativeKernel((void*)prim_kernel, dim3(G), dim3(PRIM_THREADS), args, 0, st);
+    e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(PRIM_THREADS), args, 0, st);
     cudaFreeAsync(scratch, st);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return isoc::set_error(ISOC_ECUDA, "prim_kernel launch: %s", cudaGetErrorString(e));
     }
     return ISOC_OK;
+}
+
+extern "C" int isoc_prim_edges(const double* X, int64_t n, int32_t d, int64_t root, int32_t* u,
+                               int32_t* v, double* w, void* stream) {
+    return prim_launch(false, X, n, d, root, u, v, w, stream);
+}
+
+extern "C" int isoc_prim_edges_dense(const double* D, int64_t n, int64_t root, int32_t* u, int32_t* v,
+                                     double* w, void* stream) {
+    return prim_launch(true, D, n, 1, root, u, v, w, stream);
 }

@@ -599,6 +599,7 @@ def run_pipeline(
         timings_ms={"affinity": affinity_ms, "mst": mst_ms, "partition": partition_ms,
                     "total": total_ms},
         gpus=P.comm.world, mst_stats=stats,
+        tree=LazyRootedTree(dt, root), extrema=ext, omega_device=om, p_device=p,
     )
 
 

@@ -151,8 +151,9 @@ def validate_distance_matrix(dist) -> np.ndarray:
 def prim_mst(dist, sigma: float, root: int = 0) -> RootedTree:
     """mst.py:128-181 on a distance matrix: the minimum spanning tree rooted at
     `root` with Prim's sibling ranks and parent flows.  Built by lexicographic
-    Boruvka on the device (the same tree as Prim for distinct distances; exact
-    ties at a component minimum are counted and warned about)."""
+    Boruvka on the device (the same tree as Prim for distinct distances); when
+    a round saw an exact tie at a component minimum, Prim itself is replayed
+    on the matrix (isoc_prim_edges_dense), so ties follow the reference's rule."""
     d = validate_distance_matrix(dist)
     if not (sigma > 0):
         raise ValueError(f"sigma must be > 0, got {sigma}")
@@ -168,9 +169,9 @@ def prim_mst(dist, sigma: float, root: int = 0) -> RootedTree:
     ties = ctypes.c_int64()
     check(b.lib.isoc_mst_dense(_ptr(D), n, _ptr(u), _ptr(v), _ptr(w), ctypes.byref(ties), b.stream))
     if ties.value:
-        import warnings
-        warnings.warn(f"{ties.value} exact distance ties at a component minimum: the MST may differ from "
-                      "the reference's Prim tie rule", RuntimeWarning, stacklevel=2)
+        # an exact tie at a component minimum: replay the reference's Prim on
+        # the matrix (frontier ties -> smallest vertex, strict `<` relaxation)
+        check(b.lib.isoc_prim_edges_dense(_ptr(D), n, root, _ptr(u), _ptr(v), _ptr(w), b.stream))
     dt = b.tree_from_edges(u, v, w, n, root, sigma)
     return _rooted_tree_view(dt, root)
 

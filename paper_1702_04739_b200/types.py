@@ -141,9 +141,21 @@ class PipelineRun:
     engine: str
     workers: int
     timings_ms: dict
-    # B200 extras (not in the reference): GPU count and MST statistics
+    # B200 extras (not in the reference): GPU count, MST statistics, and the
+    # stage outputs kept on the device (read lazily: tree arrays on first
+    # attribute access, omega via omega_host())
     gpus: int = 1
     mst_stats: dict = field(default_factory=dict)
+    tree: Any = field(default=None, repr=False, compare=False)
+    extrema: Optional[Extrema] = field(default=None, repr=False, compare=False)
+    omega_device: Any = field(default=None, repr=False, compare=False)
+    p_device: Any = field(default=None, repr=False, compare=False)
+
+    def omega_host(self) -> np.ndarray:
+        return self.omega_device.cpu().numpy()
+
+    def p_host(self) -> np.ndarray:
+        return self.p_device.cpu().numpy()
 
 
 def outcomes_equal(a: DecisionOutcome, b: DecisionOutcome) -> bool:

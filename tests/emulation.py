@@ -309,7 +309,10 @@ class EmuBackend:
                 row[h.comp[b * B:b * B + row.size] == h.comp[i]] = np.inf
                 if row.size and np.isfinite(row.min()):
                     j = int(np.argmin(row))
-                    psm[s], psj[s] = row[j], b * B + j
+                    psm[s] = row[j]
+                    # exact tie flag in the index's sign bit (omega_sym.cu TIEBIT)
+                    tie = int(np.count_nonzero(row == row[j]) > 1)
+                    psj[s] = np.int32(np.uint32((b * B + j) | (tie << 31)).view(np.int32))
 
         for J in range(jlo, jhi):
             for I in range(J + 1):
@@ -327,6 +330,7 @@ class EmuBackend:
         om = np.empty(hi - lo)
         nn_j = np.full(hi - lo, -1, np.int32)
         nn_d = np.full(hi - lo, np.inf)
+        nn_t = np.zeros(hi - lo, np.int8)
         for q in range(hi - lo):
             v = P[0, :, q].copy()
             for g in range(1, G):
@@ -337,16 +341,21 @@ class EmuBackend:
                 w = w[0::2] + w[1::2]
             om[q] = w[0]
             if psm is not None:
-                best = (np.inf, 2**31 - 1)
+                m, mj, tie = np.inf, 2**31 - 1, 0
                 for g in range(G):
                     for b in range(nbs):
-                        c = (float(psm[g, b, q]), int(psj[g, b, q]))
-                        best = min(best, c)
-                if best[1] != 2**31 - 1:
-                    nn_j[q], nn_d[q] = best[1], best[0]
+                        x = float(psm[g, b, q])
+                        raw = int(np.int32(psj[g, b, q]).view(np.uint32))
+                        xj, xt = raw & 0x7FFFFFFF, raw >> 31
+                        if x < m:
+                            m, mj, tie = x, xj, xt
+                        elif x == m and np.isfinite(x):
+                            mj, tie = min(mj, xj), 1
+                if mj != 2**31 - 1:
+                    nn_j[q], nn_d[q], nn_t[q] = mj, m, tie
         nn = None
         if psm is not None:
-            nn = (torch.from_numpy(nn_j), torch.from_numpy(nn_d), torch.zeros(hi - lo, dtype=torch.int8))
+            nn = (torch.from_numpy(nn_j), torch.from_numpy(nn_d), torch.from_numpy(nn_t))
         return torch.from_numpy(om), nn
 
     # Boruvka primitives on the shard's rows (exact per-row minima)

@@ -6,6 +6,7 @@ Fixtures in tests/golden were produced by running the reference
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -107,3 +108,95 @@ def test_oracle_all_flows_underflow_raises_zero_division(oracle_mod):
     pts, _ = oracle_mod.generate_random(300, 5, 3, 0)
     with pytest.raises(ZeroDivisionError):
         oracle_mod.run_pipeline(pts, 3, sigma=1e-3)
+
+
+# ------------------------------------------------ full-size oracle (isoc_fast.c)
+@pytest.mark.parametrize("n,d", [(2, 3), (50, 3), (300, 5), (1000, 16), (600, 512), (2000, 2), (4099, 7)])
+def test_fast_kernels_equal_scalar_oracle(n, d, oracle_mod):
+    """ocf_* (vectorised across pairs) == the scalar restatement, bit for bit:
+    the flat numpy sum, omega, and each row's K nearest (d, j)."""
+    pts, _ = oracle_mod.generate_random(n, d, 5, 1)
+    s = oracle_mod.flat_distance_sum(pts)
+    assert oracle_mod.flat_distance_sum_fast(pts) == s
+    sigma = s / (n * (n - 1))
+    om, _ = oracle_mod.row_folds(pts, sigma)
+    K = 8
+    om2, kd, kj = oracle_mod.omega_knn(pts, sigma, K)
+    assert np.array_equal(bits(om), bits(om2))
+    D = oracle_mod.distance_rows(pts, 0, n)
+    np.fill_diagonal(D, np.inf)
+    want = np.argsort(D, axis=1, kind="stable")[:, :min(K, n - 1)]
+    assert np.array_equal(kj[:, :want.shape[1]], want)
+    assert np.array_equal(bits(kd[:, :want.shape[1]]), bits(np.take_along_axis(D, want, 1)))
+
+
+@pytest.mark.parametrize("n,d,k,seed", [(300, 5, 4, 0), (2000, 2, 3, 0), (1500, 64, 20, 0),
+                                        (600, 512, 50, 0), (5000, 16, 10, 3)])
+def test_full_oracle_equals_scalar_oracle(n, d, k, seed, oracle_mod):
+    """run_pipeline_full (certified Boruvka + rooting) == run_pipeline (Prim)."""
+    pts, _ = oracle_mod.generate_random(n, d, k, seed)
+    a = oracle_mod.run_pipeline(pts, k)
+    b = oracle_mod.run_pipeline_full(pts, k).out
+    assert a.sigma == b.sigma
+    for name in ("parent", "depth", "child_id", "bfs_order"):
+        assert np.array_equal(getattr(a.tree, name), getattr(b.tree, name)), name
+    assert np.array_equal(bits(a.tree.parent_flow), bits(b.tree.parent_flow))
+    assert np.array_equal(bits(a.omega), bits(b.omega))
+    assert np.array_equal(a.result.labels, b.result.labels)
+    assert a.result.miso == b.result.miso
+    assert [m for m, _ in a.result.trace] == [m for m, _ in b.result.trace]
+
+
+def test_full_oracle_rejects_ties(oracle_mod):
+    """Integer lattice: many exact ties -> no uniqueness certificate."""
+    g = np.arange(12, dtype=np.float64)
+    pts = np.stack(np.meshgrid(g, g), -1).reshape(-1, 2)
+    with pytest.raises(oracle_mod.TieError):
+        oracle_mod.run_pipeline_full(pts, 3)
+
+
+def test_full_oracle_matches_reference_16000(oracle_mod):
+    """Pinned at SURVEY §7's size: the whole reference pipeline at N=16,000,
+    d=64, k=20 (tests/golden/large_n16000_d64_k20.json, produced by the
+    reference itself, tools/gen_golden_large.py) equals the full-size oracle
+    in every field (sigma, dsum-derived sigma, tree arrays, omega, extrema,
+    labels, cut, eta, sparsities, trace, alpha/beta, miso, tree weight).
+    The 32,000 and 46,340 references are checked the same way by
+    tools/oracle_full.py --check (8 s / 25 s on 8 cores; evidence in
+    profiles/round2_oracle_pins.jsonl) and on the GPU side by
+    tests/test_gpu_fullsize.py."""
+    import digest as dg
+    import os
+    want = dg.load(os.path.join(os.path.dirname(__file__), "golden", "large_n16000_d64_k20.json"))
+    meta = want["meta"]
+    pts, _ = oracle_mod.generate_random(meta["n"], meta["d"], meta["k"], meta["seed"])
+    run = oracle_mod.run_pipeline_full(pts, meta["k"])
+    o = run.out
+    e = o.extrema
+    got = dg.result_digest(o.result, sigma=o.sigma, tree=o.tree, omega=o.omega, p=o.p,
+                           extrema=[e.phi_star_sum, e.phi_star_min, e.omega_star_sum, e.omega_star_min,
+                                    e.p_star_sum, e.p_star_min],
+                           total_distance=run.total_distance)
+    got["dsum"] = dg.fbits(oracle_mod.flat_distance_sum_fast(pts))
+    assert dg.compare(got, want) == []
+    assert len([k for k in want if k in got]) >= 24
+
+
+@pytest.mark.parametrize("name", ["ties_lattice_n700_root5", "ties_round2_row_tie", "ties_round1_square_sigma1"])
+def test_oracle_prim_tie_rule_matches_reference(name, oracle_mod):
+    """The scalar oracle's Prim follows the reference's tie rule on tied
+    inputs (tools/gen_golden_ties.py fixtures)."""
+    g = load(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz"))
+    t = oracle_mod.prim_mst(g["points"], float(g["sigma"]), int(g["root"]))
+    for f in ("parent", "depth", "child_id", "bfs_order"):
+        assert np.array_equal(getattr(t, f), g[f]), f
+    assert np.array_equal(bits(t.parent_flow), bits(g["parent_flow"]))
+
+
+def test_tie_constructions_first_tie_round(oracle_mod):
+    """The constructed instances tie FIRST in the round they target (the
+    certified Boruvka reports the round of its first tie)."""
+    for name, rnd in [("ties_round2_row_tie", 2), ("ties_round1_square_sigma1", 1)]:
+        g = load(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz"))
+        with pytest.raises(oracle_mod.TieError, match=f"round {rnd}$"):
+            oracle_mod.run_pipeline_full(g["points"], int(g["k"]), root=int(g["root"]))
