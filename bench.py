@@ -11,9 +11,19 @@ generator semantics (dataset.py:140-168, PCG64 seed 0).
 
 Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under
 torch.distributed.run (one process per GPU, rows sharded, NCCL MIN
-all-reduce of the Boruvka keys).  --impl reference times the reference's
-algorithm (the CPU oracle restatement, all host threads) on a bounded
-row sample of the same workload.
+all-reduce of the Boruvka keys).  `--gpus N` without WORLD_SIZE re-launches
+itself under torch.distributed.run with N ranks (NCCL_DEBUG=INFO, INIT).
+
+--impl reference times the reference's algorithm -- the CPU oracle port
+(oracle/: scipy-order distances, numpy pairwise sigma, Prim, pow2 omega
+folds, the bisection), all host threads -- on the same workload: directly
+when N <= 46,340 (the reference's own dense cap), else on a measured ladder
+N in {16,000, 32,000, 46,340} at the config's d with each phase fitted
+(N^2: sigma, Prim, omega; N: partition) and extrapolated to N.
+
+After the timed region the GPU result is compared bit for bit with the
+committed oracle fixture of the config (tests/golden/full_<config>.json,
+tools/oracle_full.py): "parity" in the JSON line.
 """
 from __future__ import annotations
 
@@ -124,24 +134,105 @@ def peaks():
 
 
 # ------------------------------------------------------------- CPU side
-def cpu_sample(X: np.ndarray, rows: int, threads: int):
-    """Reference algorithm's O(n^2) per-point work on a bounded row sample.
+LADDER = (16_000, 32_000, 46_340)   # up to the reference's dense cap (affinity.py:139-143)
+PHASES_N2 = ("sigma", "prim", "omega")
 
-    For `rows` points the CPU oracle (isoc_oracle.c, the reference's exact
-    operation order) computes each point's full distance row (scipy order)
-    and its full omega row (glibc exp + pow2 fold) -- the per-point work of
-    distance_matrix/auto_sigma, prim_mst's relaxation and vertex_weights.
-    Returns seconds for the sample; points/s = rows / seconds.
-    """
+
+def oracle_pipeline_timed(orc, X: np.ndarray, k: int) -> dict:
+    """One run of the reference pipeline's algorithm on the host (the oracle
+    port, pipeline.py:41-104 stage order), per-phase wall seconds:
+    sigma = distance sum in scipy/numpy order (affinity.py:124-158, 233-241),
+    prim = Prim with the reference's tie rule + flows + BFS (mst.py:128-181),
+    omega = vertex_weights (affinity.py:175-201), partition = extrema +
+    bisection + labels + cost (isoperim.py:222-308)."""
+    t = {}
+    t0 = time.perf_counter()
+    sig = orc.auto_sigma_fast(X)
+    t["sigma"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    tree = orc.prim_mst(X, sig, 0)
+    t["prim"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    omega, _, _ = orc.omega_knn(X, sig, 1)
+    t["omega"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    p = np.zeros(X.shape[0])
+    orc.run_bisection(tree, omega, p, orc.extrema(tree, omega, p), k)
+    t["partition"] = time.perf_counter() - t0
+    t["total"] = sum(t.values())
+    return t
+
+
+def fit_ladder(points: list, n: int) -> dict:
+    """Least-squares through the origin per phase: N^2 phases c = sum(t N^2) /
+    sum(N^4); the partition c = sum(t N) / sum(N^2).  Returns the
+    coefficients and the extrapolated per-phase seconds at n."""
+    fit, extra = {}, {}
+    for ph in PHASES_N2 + ("partition",):
+        pw = 2 if ph in PHASES_N2 else 1
+        num = sum(pt[ph] * pt["n"] ** pw for pt in points)
+        den = sum(pt["n"] ** (2 * pw) for pt in points)
+        fit[ph] = num / den
+        extra[ph] = fit[ph] * n ** pw
+    return {"coef_s_per_Npow": fit, "extrapolated_s": extra, "total_s": sum(extra.values())}
+
+
+def cpu_reference(n: int, d: int, k: int, sizes, reps: int, threads: int, warmup: int = 1) -> dict:
+    """Time the oracle port of the reference path on the host.  N <= 46,340:
+    the workload itself, `reps` times (median).  Larger N: the ladder `sizes`
+    at the same d and k, then the per-phase fit extrapolated to N."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
 
+    orc.build()
     orc.lib().oc_set_threads(threads)
-    n = X.shape[0]
-    t0 = time.perf_counter()
-    orc.distance_rows(X, 0, rows)          # sigma / Prim rows
-    orc.row_folds(X, 1.0, 0.0, 0, rows)    # omega rows
-    return time.perf_counter() - t0
+    Xw, _ = orc.generate_random(min(n, 4000), d, k, 1)
+    for _ in range(max(0, warmup)):
+        oracle_pipeline_timed(orc, Xw, k)
+    if n <= LADDER[-1]:
+        X, _ = orc.generate_random(n, d, k, 0)
+        runs = [oracle_pipeline_timed(orc, X, k) for _ in range(max(1, reps))]
+        tot = statistics.median(r["total"] for r in runs)
+        return {"seconds": tot, "direct": True, "runs": [round(r["total"], 4) for r in runs],
+                "phases_s": {ph: round(statistics.median(r[ph] for r in runs), 4)
+                             for ph in PHASES_N2 + ("partition",)},
+                "sample": f"the whole workload (N={n}) run directly, median of {len(runs)}"}
+    points = []
+    for m in sizes:
+        X, _ = orc.generate_random(m, d, k, 0)
+        t = oracle_pipeline_timed(orc, X, k)
+        t["n"] = m
+        points.append(t)
+    fit = fit_ladder(points, n)
+    return {"seconds": fit["total_s"], "direct": False,
+            "ladder": [{kk: (round(v, 4) if isinstance(v, float) else v) for kk, v in pt.items()}
+                       for pt in points],
+            "fit": {"model": "N^2 for sigma, Prim, omega; N for the partition (least squares)",
+                    "coef_s_per_Npow": fit["coef_s_per_Npow"],
+                    "extrapolated_s": {kk: round(v, 2) for kk, v in fit["extrapolated_s"].items()}},
+            "sample": f"oracle port of the whole reference pipeline at N in {list(sizes)} (d={d}, k={k}), "
+                      f"phases fitted and extrapolated to N={n}"}
+
+
+def cpu_tree_reference(n: int, k: int, sizes) -> dict:
+    """C5 host baseline: the oracle's tree phase (tree_from_parent_list +
+    extrema + bisection; reference decide is sequential, isoperim.py:82-144)
+    on a ladder of the same generator, fitted linearly in N."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+
+    orc.build()
+    pts = []
+    for m in sizes:
+        parent, flows, omega, p = orc.random_tree_instance(m, 0)
+        t0 = time.perf_counter()
+        orc.solve_tree(parent, flows, omega, p, k)
+        pts.append({"n": m, "seconds": time.perf_counter() - t0})
+    c = sum(q["seconds"] * q["n"] for q in pts) / sum(q["n"] ** 2 for q in pts)
+    return {"seconds": c * n, "ladder": [{"n": q["n"], "seconds": round(q["seconds"], 3)} for q in pts],
+            "fit": {"model": "linear in N", "coef_s_per_vertex": c},
+            "sample": f"oracle tree phase at N in {list(sizes)} (same generator, k={k}), fitted linearly "
+                      f"and extrapolated to N={n}; single thread (the reference decide is sequential)"}
 
 
 def pkg_generate_random(n, d, k, seed):
@@ -167,35 +258,43 @@ def synthetic_tree(n: int, seed: int):
     return parent, flows, omega, np.zeros(n, dtype=np.float64)
 
 
+def workload_label(args, n, d, k) -> str:
+    if args.config == "c5":
+        return f"c5 tree phase N={n} k={k}"
+    return f"{args.config} blobs N={n} d={d} k={k}"
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    print(f"bench reference arm: rank {rank}/{world}", file=sys.stderr, flush=True)
     if rank != 0:
         return
-    n, d, k = workload(args)
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as orc
-
-    orc.build()
-    X, _ = orc.generate_random(n, d, k, 0)
     threads = os.cpu_count() or 1
-    rows = args.cpu_sample_rows or max(8, int(2.0e9 / (n * max(d, 8))))
-    rows = min(rows, n)
-    for _ in range(max(0, args.warmup)):
-        cpu_sample(X, max(1, rows // 8), threads)
-    times = [cpu_sample(X, rows, threads) for _ in range(max(1, args.steps))]
-    sec = statistics.median(times)
-    val = rows / sec
+    if args.config == "c5":
+        n = args.n or 50_000_000
+        k = args.k or 100
+        ref = cpu_tree_reference(n, k, (1_000_000, 2_000_000, 4_000_000))
+        metric, unit, cores = "tree-phase vertices/sec (C5: random spanning tree, 50M vertices, k=100)", \
+            "vertices/s", 1
+        config = {"workload": workload_label(args, n, 0, k), "n": n, "k": k}
+    else:
+        n, d, k = workload(args)
+        ref = cpu_reference(n, d, k, LADDER, max(1, args.steps), threads, args.warmup)
+        metric, unit, cores = METRIC, "points/s", threads
+        config = {"workload": workload_label(args, n, d, k), "n": n, "d": d, "k": k}
+    val = n / ref["seconds"]
     line = {
-        "impl": "reference", "metric": METRIC, "value": val, "unit": "points/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3 * n / rows,
+        "impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ref["seconds"] * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (generate_random PCG64 seed 0)",
-        "config": {"workload": f"c3-shaped blobs N={n} d={d} k={k}", "n": n, "d": d, "k": k},
-        "cpu_baseline": {"value": val, "unit": "points/s", "cores": threads, "kind": "port",
-                         "sample": f"{rows} of {n} points: exact distance row + omega row each "
-                                   f"(oracle/isoc_oracle.c, OpenMP {threads} threads); "
-                                   "extrapolated per point"},
-        "e2e": {"value": val, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic (generate_random PCG64 seed 0)" if args.config != "c5" else
+                "synthetic random recursive tree (PCG64 seed 0)",
+        "config": config,
+        "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "port",
+                         "sample": ref["sample"], **{kk: v for kk, v in ref.items()
+                                                     if kk in ("ladder", "fit", "runs", "phases_s")}},
+        "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -266,36 +365,86 @@ def tree_phase_bench(args):
                             "so the measured DRAM traffic is lower; level-synchronous (grid barriers per level), "
                             "latency rather than bandwidth bounds it"}
     # CPU baseline: the oracle's tree phase (reference operation order) on a
-    # 1M-vertex tree of the same generator, per vertex
+    # ladder of trees of the same generator, fitted linearly in N
     cpu = None
     if not args.no_cpu_baseline:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        import oracle as orc
-
-        m = 1_000_000
-        cp, cf, co, cpp = synthetic_tree(m, 0)
-        t1 = time.perf_counter()
-        orc.solve_tree(cp, cf, co, cpp, k)
-        cs = time.perf_counter() - t1
-        cpu = {"value": m / cs, "unit": "vertices/s", "cores": 1, "kind": "port",
-               "sample": f"{m}-vertex random recursive tree (same generator), tree_from_parent_list + extrema "
-                         "+ bisection in oracle/isoc_oracle.c (single thread)"}
+        ref = cpu_tree_reference(n, k, (500_000, 1_000_000, 2_000_000))
+        cpu = {"value": n / ref["seconds"], "unit": "vertices/s", "cores": 1, "kind": "port",
+               "sample": ref["sample"], "ladder": ref["ladder"], "fit": ref["fit"]}
+    tree = pkg.tree_from_parent_list(parent, flows)
+    ext = pkg.extrema(tree, w)
+    res = pkg.par_solve_miso(tree, w, ext, k)
+    parity = fixture_parity("c5", n, 0, k, None, (res, tree, omega, ext))
     print(json.dumps({
         "metric": "tree-phase vertices/sec (C5: random spanning tree, 50M vertices, k=100)",
         "value": n * args.steps / el, "unit": "vertices/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic random recursive tree (PCG64 seed 0), flows 1-U, omega 2-1.9U, p=0",
-        "config": {"workload": f"c5 tree phase N={n} k={k}", "n": n, "k": k},
+        "config": {"workload": workload_label(args, n, 0, k), "n": n, "k": k},
         "iterations": res.iterations, "miso": res.miso, "kernels": kernels, "roofline": roofline,
-        "cpu_baseline": cpu,
+        "cpu_baseline": cpu, "parity": parity,
         "e2e": {"value": n * args.steps / el, "unit": "vertices/s",
                 "h2d_bytes_per_step": n * 24, "d2h_bytes_per_step": n * 17},
         "gpu_launches": int(launches), "clocks": clocks}), flush=True)
 
 
+def fixture_parity(config: str, n: int, d: int, k: int, run, tree_res=None) -> dict:
+    """Bitwise comparison with the committed oracle fixture of this config
+    (tests/golden/full_<config>.json; tools/oracle_full.py), outside the
+    timed region.  Points configs compare sigma, the tree arrays and MST
+    edge set, omega, extrema, labels, cut, eta, sparsities, trace,
+    iterations, alpha/beta and miso."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import digest as dg
+    path = os.path.join(ROOT, "tests", "golden", f"full_{config}.json")
+    if not os.path.exists(path):
+        return {"status": "no-fixture", "fixture": os.path.relpath(path, ROOT)}
+    want = dg.load(path)
+    m = want["meta"]
+    if m.get("n") != n or m.get("k") != k or (config != "c5" and m.get("d") != d):
+        return {"status": "no-fixture", "fixture": os.path.relpath(path, ROOT), "why": "different n/d/k"}
+    if config == "c5":
+        res, tree, omega, ext = tree_res
+        got = dg.result_digest(res, tree=tree, omega=omega,
+                               extrema=[ext.phi_star_sum, ext.phi_star_min, ext.omega_star_sum,
+                                        ext.omega_star_min, ext.p_star_sum, ext.p_star_min])
+    else:
+        e = run.extrema
+        got = dg.result_digest(run.result, sigma=run.sigma, tree=run.tree, omega=run.omega_host(),
+                               p=run.p_host(),
+                               extrema=[e.phi_star_sum, e.phi_star_min, e.omega_star_sum, e.omega_star_min,
+                                        e.p_star_sum, e.p_star_min])
+    keys = [kk for kk in want if kk in got and kk != "meta"]
+    bad = dg.compare(got, want, keys)
+    return {"status": "fixture-match" if not bad else "MISMATCH", "fields_compared": len(keys),
+            "differs": bad, "fixture": os.path.relpath(path, ROOT)}
+
+
+def self_launch(args) -> bool:
+    """--gpus N > 1 without a torch.distributed environment: re-run this
+    command under torch.distributed.run with N ranks on this node."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+               NCCL_DEBUG_SUBSYS=os.environ.get("NCCL_DEBUG_SUBSYS", "INIT"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    print("bench: self-launch " + " ".join(cmd), file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd, env=env))
+
+
 def main():
     args = parse()
+    self_launch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; launch with torchrun "
+                 f"--nproc-per-node {args.gpus} or without WORLD_SIZE")
     if args.impl == "reference":
         return reference_arm(args)
     if args.config == "c5":
@@ -490,13 +639,15 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # bounded sample (~10-30 s of host work): the oracle port of the whole
+        # reference pipeline at N=16,000 (or the workload itself when smaller),
+        # per phase, extrapolated with the N^2 / N phase model
         threads = os.cpu_count() or 1
-        rows = args.cpu_sample_rows or max(8, int(2.0e9 / (n * max(d, 8))))
-        rows = min(rows, n)
-        sec = cpu_sample(X, rows, threads)
-        cpu = {"value": rows / sec, "unit": "points/s", "cores": threads, "kind": "port",
-               "sample": f"{rows} of {n} points: exact distance row + omega row each "
-                         f"(oracle/isoc_oracle.c, OpenMP {threads} threads); extrapolated per point"}
+        ref = cpu_reference(n, d, k, (16_000,), 1, threads, 0)
+        cpu = {"value": n / ref["seconds"], "unit": "points/s", "cores": threads, "kind": "port",
+               "sample": ref["sample"], **{kk: v for kk, v in ref.items() if kk in ("ladder", "fit", "phases_s")}}
+
+    parity = fixture_parity(args.config, n, d, k, run)
 
     if rank == 0:
         line = {
@@ -504,8 +655,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generate_random PCG64 seed 0, Gaussian blobs)",
-            "config": {"workload": f"c3 blobs N={n} d={d} k={k}" if args.config == "c3"
-                       else f"{args.config} blobs N={n} d={d} k={k}",
+            "config": {"workload": workload_label(args, n, d, k),
                        "n": n, "d": d, "k": k, "parallelism": (f"symmetric super-tile ranges x{world} (rows owned per rank)" if world > 1 else "one GPU, symmetric super-tiles"),
                        "l2": "inputs larger than L2 (N*d*8 bytes) and an n^2 stream per step"},
             "mst_phase_ms": statistics.median(mst_ms) if mst_ms else None,
@@ -518,6 +668,7 @@ def main():
                                       "hbm_gbs_file": peaks().get("hbm_gbs")},
             "filter": "tcgen05 3xFP16 split" if use_tc else "FP32 FFMA",
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches),
