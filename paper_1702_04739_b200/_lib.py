@@ -89,6 +89,7 @@ SIGNATURES = {
     "isoc_mst_round_finish": (ctypes.c_int, [P, P, P, PI64, PI64, PI64]),
     "isoc_mst_edges": (ctypes.c_int, [P, P, P, P]),
     "isoc_prim_edges": (ctypes.c_int, [P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, P, P, P, P]),
+    "isoc_mst_filter_stats": (ctypes.c_int, [P, PI64, PI64, PI64]),
     "isoc_prim_edges_dense": (ctypes.c_int, [P, ctypes.c_int64, ctypes.c_int64, P, P, P, P]),
     "isoc_mst_destroy": (None, [P]),
     "isoc_tree_from_edges": (ctypes.c_int, [P, P, P, I64, I64, D, P, ctypes.POINTER(P)]),

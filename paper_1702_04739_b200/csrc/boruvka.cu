@@ -293,6 +293,63 @@ __global__ void candidate_kernel(const double* __restrict__ X, int d, const floa
     }
 }
 
+// ------------------------------------------------ candidate lists (tc filter)
+// A row's list holds its FILTER_LIST_K best (a, j) over the columns that were
+// in other components when the filter last ran for its block, plus lb <= a of
+// every unlisted column.  Components only merge, so a listed column that is
+// still in another component is still a valid candidate, and every column
+// not listed has a >= lb.  Per row: a1/j1 = the first still-external entry,
+// a2 = min(next still-external entry, lb) -- the (a1, j1, a2) contract of
+// the filter kernels, consumed unchanged by comp_bound / candidate_kernel.
+// No still-external entry: a1 = inf and the row's lower bound lbo = lb.
+__global__ void list_select_kernel(const float* __restrict__ la, const int32_t* __restrict__ lj,
+                                   const float* __restrict__ lb, const int32_t* __restrict__ comp,
+                                   int64_t lo, int64_t hi, float* __restrict__ a1, int32_t* __restrict__ j1,
+                                   float* __restrict__ a2, float* __restrict__ lbo) {
+    const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hi) return;
+    const int64_t li = i - lo;
+    const int32_t c = comp[i];
+    float f1 = INFINITY, f2 = INFINITY;
+    int32_t g1 = -1;
+    int found = 0;
+#pragma unroll
+    for (int p = 0; p < FILTER_LIST_K; ++p) {
+        const int32_t j = lj[li * FILTER_LIST_K + p];
+        if (j < 0 || found == 2) continue;
+        if (comp[j] == c) continue;
+        const float v = la[li * FILTER_LIST_K + p];
+        if (found == 0) { f1 = v; g1 = j; } else { f2 = v; }
+        ++found;
+    }
+    const float b = lb[li];
+    a1[li] = f1;
+    j1[li] = g1;
+    a2[li] = fminf(f2, b);
+    lbo[li] = found ? INFINITY : b;
+}
+
+// Rows whose list has no external entry but whose lower bound does not rule
+// them out of their component's minimum (lb - E <= B, or no bound yet) flag
+// their 256-row filter block for a refresh.
+__global__ void list_refresh_kernel(const float* __restrict__ lbo, const float* __restrict__ rad,
+                                    const int32_t* __restrict__ comp, int64_t lo, int64_t hi,
+                                    const uint32_t* __restrict__ rmax_bits, float cd, float cabs,
+                                    const uint32_t* __restrict__ compB, int32_t* __restrict__ blk_flag,
+                                    int32_t* __restrict__ nflag, int32_t* __restrict__ rows_list) {
+    const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hi) return;
+    const float b = lbo[i - lo];
+    if (!(b < INFINITY)) return;
+    const float E = row_bound(rad[i], __uint_as_float(*rmax_bits), cd, cabs);
+    const float B = ordered_to_float(compB[comp[i]]);
+    if (__fsub_rd(b, E) > B) return;   // (false when B is NaN: no bound yet)
+    const int64_t blk = (i / 128 - lo / 128) / 2;
+    rows_list[atomicAdd(nflag + 1, 1)] = (int32_t)i;           // rows (any order: each row's
+                                                               // list is computed on its own)
+    if (blk_flag[blk] == 0 && atomicExch(&blk_flag[blk], 1) == 0) atomicAdd(nflag, 1);   // blocks
+}
+
 // Exact rescan of one row per CTA: min (d, j) over other-component columns,
 // plus whether the minimum is attained twice.  Each thread keeps four
 // independent distance chains in flight (columns j, j+T, j+2T, j+3T).
@@ -741,6 +798,31 @@ cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float
     cudaFreeAsync(pm1, st);
     cudaFreeAsync(pm2, st);
     cudaFreeAsync(pj, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_list_select(const float* la, const int32_t* lj, const float* lb, const int32_t* comp,
+                               int64_t lo, int64_t hi, float* a1, int32_t* j1, float* a2, float* lbo,
+                               cudaStream_t st) {
+    if (hi <= lo) return cudaSuccess;
+    list_select_kernel<<<blocks_for(hi - lo, 256), 256, 0, st>>>(la, lj, lb, comp, lo, hi, a1, j1, a2, lbo);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_list_refresh(const float* a1, const float* lbo, const float* rad, const int32_t* comp,
+                                int64_t n, int64_t lo, int64_t hi, const uint32_t* rmax_bits, float cd,
+                                float cabs, uint32_t* compB, int32_t* blk_flag, int64_t nblk, int32_t* nflag,
+                                int32_t* rows_list, cudaStream_t st) {
+    const int64_t rows = hi - lo;
+    if (rows <= 0) return cudaSuccess;
+    cudaMemsetAsync(compB, 0xff, (size_t)n * sizeof(uint32_t), st);
+    cudaMemsetAsync(blk_flag, 0, (size_t)nblk * sizeof(int32_t), st);
+    cudaMemsetAsync(nflag, 0, 2 * sizeof(int32_t), st);
+    comp_bound_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(a1, rad, comp, lo, hi, rmax_bits, cd, cabs, compB);
+    list_refresh_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(lbo, rad, comp, lo, hi, rmax_bits, cd, cabs,
+                                                                compB, blk_flag, nflag, rows_list);
+    note_launch(2);
     return cudaGetLastError();
 }
 

@@ -336,13 +336,22 @@ struct isoc_mst {
     int32_t *succ, *succ2;
     int32_t *eu, *ev;
     double* ed;
+    // tc filter candidate lists (FILTER_LIST_K per row) and block refresh flags
+    float *la, *lb, *lbo;
+    int32_t* lj;
+    int32_t *blk_flag, *refresh_rows;
+    uint8_t* imgA;
+    int64_t nblk;
+    int lists_valid;
+    int64_t filter_blocks_run, filter_blocks_total, filter_rows_refreshed;
 };
 
 static void mst_free(isoc_mst* h) {
     if (!h) return;
     void* ptrs[] = {h->img, h->Y, h->ny, h->rad, h->centre, h->rmax, h->comp, h->a1, h->a2, h->j1,
                     h->compB, h->cand_d, h->cand_j, h->cand_state, h->cand_tie, h->rescan_list,
-                    h->counters, h->succ, h->succ2, h->eu, h->ev, h->ed};
+                    h->counters, h->succ, h->succ2, h->eu, h->ev, h->ed, h->la, h->lb, h->lbo, h->lj,
+                    h->blk_flag, h->refresh_rows, h->imgA};
     for (void* p : ptrs)
         if (p) cudaFreeAsync(p, h->st);
     delete h;
@@ -423,6 +432,14 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
         h->cabs = (float)(ldexp(1.0, -22 - s) * 8.0 * 2.0 * (kd / 64.0));
         MCK(dalloc(&h->img, tc_image_bytes(n, d), h->st));
         MCK(launch_tc_image(h->Y, h->npad, d, scale, n, h->img, h->st));
+        MCK(dalloc(&h->la, h->rows * FILTER_LIST_K, h->st));
+        MCK(dalloc(&h->lj, h->rows * FILTER_LIST_K, h->st));
+        MCK(dalloc(&h->lb, h->rows, h->st));
+        MCK(dalloc(&h->lbo, h->rows, h->st));
+        h->nblk = filter_tc_blocks(lo, hi);
+        MCK(dalloc(&h->blk_flag, h->nblk, h->st));
+        MCK(dalloc(&h->refresh_rows, h->rows, h->st));
+        MCK(dalloc(&h->imgA, tc_image_bytes((h->rows + 255) / 256 * 256, d), h->st));
     } else {
         h->cabs = 0.f;
     }
@@ -438,10 +455,40 @@ int isoc_mst_round_local(isoc_mst* h, int use_nn, const int32_t* nn_j, const dou
         CK(launch_nn_candidates(nn_j, nn_d, nn_tie, h->rows, h->cand_d, h->cand_j, h->cand_state,
                                 h->cand_tie, st));
     } else {
-        if (h->use_tc)
-            CK(launch_filter_tc(h->img, h->ny, h->comp, h->n, h->d, h->lo, h->hi, h->kscale, h->a1, h->j1, h->a2,
-                                st));
-        else
+        if (h->use_tc) {
+            // candidate lists: the first filter round scans every block; later
+            // rounds read each row's minimum from its list and re-run the
+            // filter only for blocks holding a row whose list ran out while it
+            // may still hold its component's minimum
+            if (!h->lists_valid) {
+                CK(launch_filter_tc(h->img, h->ny, h->comp, h->n, h->d, h->lo, h->hi, h->kscale, h->la, h->lj,
+                                    h->lb, nullptr, nullptr, 0, nullptr, st));
+                h->lists_valid = 1;
+                h->filter_blocks_run += h->nblk;
+                h->filter_blocks_total += h->nblk;
+                CK(launch_list_select(h->la, h->lj, h->lb, h->comp, h->lo, h->hi, h->a1, h->j1, h->a2, h->lbo,
+                                      st));
+            } else {
+                CK(launch_list_select(h->la, h->lj, h->lb, h->comp, h->lo, h->hi, h->a1, h->j1, h->a2, h->lbo,
+                                      st));
+                CK(launch_list_refresh(h->a1, h->lbo, h->rad, h->comp, h->n, h->lo, h->hi, h->rmax, h->cd,
+                                       h->cabs, h->compB, h->blk_flag, h->nblk, h->counters + 5,
+                                       h->refresh_rows, st));
+                int32_t nf[2] = {0, 0};   // flagged blocks, rows
+                CK(cudaMemcpyAsync(nf, h->counters + 5, sizeof nf, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                h->filter_blocks_total += h->nblk;
+                h->filter_rows_refreshed += nf[1];
+                if (nf[1] > 0) {
+                    // the rows whose list ran out, gathered (row granularity)
+                    h->filter_blocks_run += (nf[1] + 255) / 256;
+                    CK(launch_filter_tc(h->img, h->ny, h->comp, h->n, h->d, h->lo, h->hi, h->kscale, h->la,
+                                        h->lj, h->lb, h->refresh_rows, h->counters + 6, nf[1], h->imgA, st));
+                    CK(launch_list_select(h->la, h->lj, h->lb, h->comp, h->lo, h->hi, h->a1, h->j1, h->a2,
+                                          h->lbo, st));
+                }
+            }
+        } else
             CK(launch_boruvka_filter(h->Y, h->ny, h->comp, h->n, h->npad, h->dp, h->lo, h->hi, h->a1,
                                      h->j1, h->a2, st));
         CK(launch_boruvka_select(h->X, h->n, h->d, h->a1, h->j1, h->a2, h->rad, h->rmax, h->cd, h->cabs,
@@ -488,6 +535,14 @@ int isoc_mst_edges(isoc_mst* h, int32_t* u, int32_t* v, double* w) {
     if (u) CK(cudaMemcpyAsync(u, h->eu, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st));
     if (v) CK(cudaMemcpyAsync(v, h->ev, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st));
     if (w) CK(cudaMemcpyAsync(w, h->ed, (size_t)cnt * 8, cudaMemcpyDeviceToDevice, h->st));
+    return ISOC_OK;
+}
+
+int isoc_mst_filter_stats(isoc_mst* h, int64_t* blocks_run, int64_t* blocks_total, int64_t* rows_refreshed) {
+    if (!h) return fail(ISOC_EINVAL, "null MST handle");
+    if (blocks_run) *blocks_run = h->filter_blocks_run;
+    if (blocks_total) *blocks_total = h->filter_blocks_total;
+    if (rows_refreshed) *rows_refreshed = h->filter_rows_refreshed;
     return ISOC_OK;
 }
 

@@ -15,7 +15,12 @@
 // (one elected lane); warps 2-9: epilogue, one thread per row reading its
 // 128 accumulator columns with tcgen05.ld and keeping (a1, j1, a2).
 // Accumulators are double buffered in TMEM (2 x 256 columns) so the MMA of
-// tile t+1 overlaps the epilogue of tile t.  d <= 64: one 64-wide K atom,
+// tile t+1 overlaps the epilogue of tile t.  Each row keeps its TC_K best
+// (a, j) in registers -- a candidate list (sorted, lexicographic (a, j)) and
+// the bound lb every unlisted column satisfies (a >= lb) -- so later Boruvka
+// rounds can take a row's minimum from its list while the listed columns
+// stay in other components, and launch the filter only for the 256-row
+// blocks (blk_flag) holding rows whose list ran out.  d <= 64: one 64-wide K atom,
 // A resident; d > 64: every stage streams one K atom of A (both row blocks)
 // and of the tile, accumulating the atoms in TMEM.
 #include <cstdint>
@@ -36,6 +41,7 @@ constexpr int TC_THREADS = 64 + 32 * TC_EPI;
 constexpr int TC_PART = 16384;      // bytes of one 128 x 64 fp16 image
 constexpr int TC_META = 8;
 constexpr int TC_MS = 4;            // metadata ring slots
+constexpr int TC_K = FILTER_LIST_K;  // candidate list length per row (kernels.h)
 
 // Resident-A layout (d <= 64: one 64-wide K atom) and streaming layout
 // (d > 64: each stage carries one K atom of both row blocks and the tile).
@@ -45,8 +51,8 @@ struct TcSmemT {
     uint8_t B[TC_STAGES][2][TC_PART];    // [stage][hi/lo]
     int32_t mcomp[TC_MS][TC_BN];         // column metadata ring (bulk-copied by the producer)
     float mnorm[TC_MS][TC_BN];
-    float xa1[2 * TC_BM], xa2[2 * TC_BM];  // second-half partials of each row
-    int32_t xj1[2 * TC_BM];
+    float xla[(TC_K + 1) * 2 * TC_BM];   // second-half lists of each row
+    int32_t xlj[(TC_K + 1) * 2 * TC_BM];
     uint64_t full[TC_STAGES];
     uint64_t empty[TC_STAGES];
     uint64_t afull;
@@ -62,8 +68,8 @@ struct TcSmemT<true> {
     uint8_t S[TC_SSTAGES][6][TC_PART];   // [stage][A blk0 hi, lo, A blk1 hi, lo, B hi, lo]
     int32_t mcomp[TC_MS][TC_BN];
     float mnorm[TC_MS][TC_BN];
-    float xa1[2 * TC_BM], xa2[2 * TC_BM];
-    int32_t xj1[2 * TC_BM];
+    float xla[(TC_K + 1) * 2 * TC_BM];
+    int32_t xlj[(TC_K + 1) * 2 * TC_BM];
     uint64_t full[TC_STAGES];
     uint64_t empty[TC_STAGES];
     uint64_t afull;
@@ -160,19 +166,53 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void tc_update(float a, int32_t j, float& a1, int32_t& j1, float& a2) {
-    const bool lt = a < a1;
-    a2 = fminf(a2, fmaxf(a, a1));
-    j1 = lt ? j : j1;
-    a1 = fminf(a1, a);
+// Each row keeps TC_KL = TC_K + 1 entries: the TC_K it reports and one more,
+// whose value is the bound lb of every column outside the list (a value
+// that falls off the end is >= it).  Branch-free insertion of (a, j) into
+// the sorted list (strict <: among equal values the earlier -- smaller --
+// column stays first).
+constexpr int TC_KL = TC_K + 1;
+__device__ __forceinline__ void list_insert(float a, int32_t j, float (&la)[TC_KL], int32_t (&lj)[TC_KL]) {
+    float x = a;
+    int32_t xj = j;
+#pragma unroll
+    for (int p = 0; p < TC_KL; ++p) {
+        const bool lt = x < la[p];
+        const float ta = la[p];
+        const int32_t tj = lj[p];
+        la[p] = lt ? x : ta;
+        lj[p] = lt ? xj : tj;
+        x = lt ? ta : x;
+        xj = lt ? tj : xj;
+    }
+}
+
+// lexicographic (a, j) insertion for merging two lists whose columns interleave
+__device__ __forceinline__ void list_insert_lex(float a, int32_t j, float (&la)[TC_KL], int32_t (&lj)[TC_KL]) {
+    float x = a;
+    int32_t xj = j;
+#pragma unroll
+    for (int p = 0; p < TC_KL; ++p) {
+        const bool lt = x < la[p] || (x == la[p] && xj >= 0 && (lj[p] < 0 || xj < lj[p]));
+        const float ta = la[p];
+        const int32_t tj = lj[p];
+        la[p] = lt ? x : ta;
+        lj[p] = lt ? xj : tj;
+        x = lt ? ta : x;
+        xj = lt ? tj : xj;
+    }
 }
 
 template <bool STREAM>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                  const int32_t* __restrict__ comp, int64_t n, int64_t row_lo, int64_t row_hi,
-                 float kscale, float* __restrict__ out_a1, int32_t* __restrict__ out_j1,
-                 float* __restrict__ out_a2, int KA) {
+                 float kscale, float* __restrict__ out_la, int32_t* __restrict__ out_lj,
+                 float* __restrict__ out_lb, const uint8_t* __restrict__ imgA,
+                 const int32_t* __restrict__ rows_map, int64_t nmap, int KA) {
+    // rows_map != nullptr: gathered mode -- the CTA's 256 rows are
+    // rows_map[256 * blockIdx.x + 0..255] (global ids, < nmap valid) and their
+    // A operands come from the gathered image imgA (built by tc_gather_kernel)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmemT<STREAM>& sm = *reinterpret_cast<TcSmemT<STREAM>*>(
         reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023)));
@@ -214,8 +254,10 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
             mbar_expect_tx(&sm.afull, 4 * TC_PART);
             for (int r = 0; r < 2; ++r) {
                 const int64_t b = (blk0 + r < nblocks_total) ? blk0 + r : nblocks_total - 1;
-                bulk_g2s(sm.A[r][0], img + (b * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.afull);
-                bulk_g2s(sm.A[r][1], img + (b * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.afull);
+                const uint8_t* asrc = rows_map ? imgA + (2 * (int64_t)blockIdx.x + r) * 2 * (int64_t)TC_PART
+                                               : img + b * 2 * (int64_t)TC_PART;
+                bulk_g2s(sm.A[r][0], asrc, TC_PART, &sm.afull);
+                bulk_g2s(sm.A[r][1], asrc + TC_PART, TC_PART, &sm.afull);
             }
           }
             int64_t q = 0;   // stage uses (streaming)
@@ -236,8 +278,11 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                     mbar_expect_tx(&sm.full[s], 6 * TC_PART);
                     for (int r = 0; r < 2; ++r) {
                         const int64_t b = (blk0 + r < nblocks_total) ? blk0 + r : nblocks_total - 1;
-                        bulk_g2s(sm.S[s][2 * r + 0], img + ((b * KA + a) * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
-                        bulk_g2s(sm.S[s][2 * r + 1], img + ((b * KA + a) * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
+                        const uint8_t* asrc =
+                            rows_map ? imgA + (((2 * (int64_t)blockIdx.x + r) * KA + a) * 2) * (int64_t)TC_PART
+                                     : img + ((b * KA + a) * 2) * (int64_t)TC_PART;
+                        bulk_g2s(sm.S[s][2 * r + 0], asrc, TC_PART, &sm.full[s]);
+                        bulk_g2s(sm.S[s][2 * r + 1], asrc + TC_PART, TC_PART, &sm.full[s]);
                     }
                     bulk_g2s(sm.S[s][4], img + ((t * KA + a) * 2 + 0) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
                     bulk_g2s(sm.S[s][5], img + ((t * KA + a) * 2 + 1) * (int64_t)TC_PART, TC_PART, &sm.full[s]);
@@ -312,11 +357,21 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
         const int r = e >> 3;
         const int hcol = (e >> 2) & 1;
         const int lrow = q * 32 + lane;
-        const int64_t row = (blk0 + r) * TC_BM + lrow;
-        const bool live = row >= row_lo && row < row_hi;
+        int64_t row;
+        bool live;
+        if (rows_map) {
+            const int64_t g = 256 * (int64_t)blockIdx.x + r * TC_BM + lrow;
+            live = g < nmap;
+            row = live ? rows_map[g] : -1;
+        } else {
+            row = (blk0 + r) * TC_BM + lrow;
+            live = row >= row_lo && row < row_hi;
+        }
         const int32_t rc = live ? comp[row] : -2;
-        float a1 = INFINITY, a2 = INFINITY;
-        int32_t j1 = -1;
+        float la[TC_KL];
+        int32_t lj[TC_KL];
+#pragma unroll
+        for (int p = 0; p < TC_KL; ++p) { la[p] = INFINITY; lj[p] = -1; }
         for (int64_t t = 0; t < ntiles; ++t) {
             const int as = (int)(t & 1);
             const int ms = (int)(t % TC_MS);
@@ -329,8 +384,8 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                 float v[32];
                 tmem_ld32(tbase + (uint32_t)(c * 32), v);
                 const int lc0 = hcol * 64 + c * 32;
-                // masked estimates and their chunk minimum; the top-2 update
-                // can only change (a1, j1, a2) if some value is below a2
+                // masked estimates and their chunk minimum; the list can only
+                // change if some value is below its last entry
                 float m = INFINITY;
 #pragma unroll
                 for (int i4 = 0; i4 < 8; ++i4) {
@@ -346,9 +401,13 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                         m = fminf(m, v[i]);
                     }
                 }
-                if (m < a2) {
+                // per value: a warp runs an insertion only when one of its 32
+                // rows has that value below its list end (a per-chunk gate
+                // would run all 32 whenever any row's chunk qualifies)
+                if (m < la[TC_KL - 1]) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) tc_update(v[i], (int32_t)(t * TC_BN + lc0 + i), a1, j1, a2);
+                    for (int i = 0; i < 32; ++i)
+                        if (v[i] < la[TC_KL - 1]) list_insert(v[i], (int32_t)(t * TC_BN + lc0 + i), la, lj);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -358,25 +417,33 @@ filter_tc_kernel(const uint8_t* __restrict__ img, const float* __restrict__ ny,
                 mbar_arrive(&sm.mempty[ms]);
             }
         }
+        // the two column halves of a row merge through shared memory (the
+        // operand stages are free once every MMA has completed: each thread
+        // waited on the last tile's tfull)
         const int slot = r * TC_BM + lrow;
+        float* xla = sm.xla;
+        int32_t* xlj = sm.xlj;
         if (hcol == 1) {
-            sm.xa1[slot] = a1;
-            sm.xa2[slot] = a2;
-            sm.xj1[slot] = j1;
+#pragma unroll
+            for (int p = 0; p < TC_KL; ++p) {
+                xla[p * 2 * TC_BM + slot] = la[p];
+                xlj[p * 2 * TC_BM + slot] = lj[p];
+            }
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(32 * TC_EPI) : "memory");
         if (hcol == 0 && live) {
-            // columns of the two halves interleave per tile: lexicographic (a, j)
-            const float b1 = sm.xa1[slot], b2 = sm.xa2[slot];
-            const int32_t bj = sm.xj1[slot];
-            const bool other = b1 < a1 || (b1 == a1 && bj >= 0 && (j1 < 0 || bj < j1));
-            const float lose = other ? a1 : b1;
-            a2 = fminf(fminf(a2, b2), lose);
-            if (other) { a1 = b1; j1 = bj; }
+#pragma unroll
+            for (int p = 0; p < TC_KL; ++p) list_insert_lex(xla[p * 2 * TC_BM + slot], xlj[p * 2 * TC_BM + slot], la, lj);
+            const float lb = la[TC_K];
+            // the row norm is added after the minimum (rounding is monotone)
             const float rn = ny[row];
-            out_a1[row - row_lo] = a1 + rn;
-            out_j1[row - row_lo] = j1;
-            out_a2[row - row_lo] = a2 + rn;
+            const int64_t li = row - row_lo;
+#pragma unroll
+            for (int p = 0; p < TC_K; ++p) {
+                out_la[li * TC_K + p] = la[p] + rn;
+                out_lj[li * TC_K + p] = lj[p];
+            }
+            out_lb[li] = lb + rn;
         }
     }
     __syncthreads();
@@ -405,6 +472,36 @@ __global__ void tc_image_kernel(const float* __restrict__ YT, int64_t npad, int 
     *reinterpret_cast<__half*>(img + ((b * KA + a) * 2 + 1) * (int64_t)TC_PART + off) = lo;
 }
 
+// Gathered A images for the rows of rows_map: row g of the gathered image is
+// row rows_map[g] of img, 16-byte chunks re-swizzled for the new row slot.
+__global__ void tc_gather_kernel(const uint8_t* __restrict__ img, const int32_t* __restrict__ rows_map,
+                                 const int32_t* __restrict__ nmap_dev, int KA, uint8_t* __restrict__ imgA) {
+    const int64_t nmap = *nmap_dev;
+    const int64_t total = (nmap + 255) / 256 * 256 * KA * 2 * 8;   // (row, atom, part, chunk)
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e & 7);
+        const int part = (int)((e >> 3) & 1);
+        const int64_t ra = e >> 4;
+        const int a = (int)(ra % KA);
+        const int64_t g = ra / KA;
+        const int rd = (int)(g % TC_BM);
+        const int64_t bd = g / TC_BM;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (g < nmap) {
+            const int64_t src = rows_map[g];
+            const int rs = (int)(src % TC_BM);
+            const int64_t bs = src / TC_BM;
+            const uint8_t* p = img + ((bs * KA + a) * 2 + part) * (int64_t)TC_PART + (rs >> 3) * 1024 +
+                               (rs & 7) * 128 + ((c ^ (rs & 7)) << 4);
+            v = *reinterpret_cast<const uint4*>(p);
+        }
+        uint8_t* q = imgA + ((bd * KA + a) * 2 + part) * (int64_t)TC_PART + (rd >> 3) * 1024 + (rd & 7) * 128 +
+                     ((c ^ (rd & 7)) << 4);
+        *reinterpret_cast<uint4*>(q) = v;
+    }
+}
+
 size_t tc_image_bytes(int64_t n, int d) {
     const int64_t nblocks = (n + TC_BM - 1) / TC_BM;
     const int KA = (d + 63) / 64;
@@ -422,28 +519,41 @@ cudaError_t launch_tc_image(const float* YT, int64_t npad, int d, float scale, i
 }
 
 cudaError_t launch_filter_tc(const uint8_t* img, const float* ny, const int32_t* comp, int64_t n, int d,
-                             int64_t lo, int64_t hi, float kscale, float* a1, int32_t* j1, float* a2,
+                             int64_t lo, int64_t hi, float kscale, float* la, int32_t* lj, float* lb,
+                             const int32_t* rows_map, const int32_t* nmap_dev, int64_t nmap, uint8_t* imgA,
                              cudaStream_t st) {
     if (hi <= lo) return cudaSuccess;
     const int KA = (d + 63) / 64;
-    const int64_t b_lo = lo / TC_BM, b_hi = (hi + TC_BM - 1) / TC_BM;
-    const unsigned grid = (unsigned)((b_hi - b_lo + 1) / 2);
+    unsigned grid = (unsigned)filter_tc_blocks(lo, hi);
+    if (rows_map) {
+        if (nmap <= 0) return cudaSuccess;
+        grid = (unsigned)((nmap + 255) / 256);
+        tc_gather_kernel<<<148 * 4, 256, 0, st>>>(img, rows_map, nmap_dev, KA, imgA);
+        note_launch();
+    }
     const int pid = prof_begin(PK_FILTER, st);
     cudaError_t e;
     if (KA == 1) {
         const size_t smem = sizeof(TcSmemT<false>) + 1024;
         e = cudaFuncSetAttribute(filter_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        filter_tc_kernel<false><<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, a1, j1, a2, 1);
+        filter_tc_kernel<false><<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, la, lj, lb,
+                                                                 imgA, rows_map, nmap, 1);
     } else {
         const size_t smem = sizeof(TcSmemT<true>) + 1024;
         e = cudaFuncSetAttribute(filter_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        filter_tc_kernel<true><<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, a1, j1, a2, KA);
+        filter_tc_kernel<true><<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, la, lj, lb,
+                                                                imgA, rows_map, nmap, KA);
     }
     prof_end(pid, st);
     note_launch();
     return cudaGetLastError();
+}
+
+int64_t filter_tc_blocks(int64_t lo, int64_t hi) {
+    const int64_t b_lo = lo / TC_BM, b_hi = (hi + TC_BM - 1) / TC_BM;
+    return (b_hi - b_lo + 1) / 2;
 }
 
 }  // namespace isoc

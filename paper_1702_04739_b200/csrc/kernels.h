@@ -93,9 +93,23 @@ cudaError_t launch_hook_contract(int32_t* comp, int64_t n, const unsigned long l
 size_t tc_image_bytes(int64_t n, int d);
 cudaError_t launch_tc_image(const float* YT, int64_t npad, int d, float scale, int64_t n, uint8_t* img,
                             cudaStream_t st);
+// candidate lists per row: FILTER_LIST_K best (a, j) + the bound of the rest
+#define FILTER_LIST_K 8
+// rows_map == nullptr: every row of [lo, hi); else the nmap rows listed
+// (device count nmap_dev), whose A operands are gathered into imgA
+// (tc_image_bytes(nmap rounded up to 256, d) bytes)
 cudaError_t launch_filter_tc(const uint8_t* img, const float* ny, const int32_t* comp, int64_t n, int d,
-                             int64_t lo, int64_t hi, float kscale, float* a1, int32_t* j1, float* a2,
+                             int64_t lo, int64_t hi, float kscale, float* la, int32_t* lj, float* lb,
+                             const int32_t* rows_map, const int32_t* nmap_dev, int64_t nmap, uint8_t* imgA,
                              cudaStream_t st);
+int64_t filter_tc_blocks(int64_t lo, int64_t hi);
+cudaError_t launch_list_select(const float* la, const int32_t* lj, const float* lb, const int32_t* comp,
+                               int64_t lo, int64_t hi, float* a1, int32_t* j1, float* a2, float* lbo,
+                               cudaStream_t st);
+cudaError_t launch_list_refresh(const float* a1, const float* lbo, const float* rad, const int32_t* comp,
+                                int64_t n, int64_t lo, int64_t hi, const uint32_t* rmax_bits, float cd,
+                                float cabs, uint32_t* compB, int32_t* blk_flag, int64_t nblk, int32_t* nflag,
+                                int32_t* rows_list, cudaStream_t st);
 cudaError_t launch_absmax(const float* v, int64_t m, uint32_t* out, cudaStream_t st);
 
 // tree.cu

@@ -287,7 +287,10 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                     for (int j = 0; j < 8; ++j) {
                         const bool ok = (!CHK || (i < rlim && LCOL(j) < clim)) && ts.comp_c[LCOL(j)] != cr;
                         const uint64_t bv = (uint64_t)__double_as_longlong(acc[i][j]);
-                        if (ok) tie_merge_bits(m, mj, bv, (int32_t)(gcb + LCOL(j)));
+                        // columns ascend within the thread: an equal value is a tie
+                        // with the (smaller) column already held
+                        if (ok && bv < m) { m = bv; mj = (int32_t)(gcb + LCOL(j)); }
+                        else if (ok && bv == m) mj |= TIEBIT;
                     }
 #pragma unroll
                     for (int off = 1; off < 8; off <<= 1) {
@@ -316,7 +319,8 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                         for (int i = 0; i < 4; ++i) {
                             const bool ok = (!CHK || (i < rlim && LCOL(j) < clim)) && ts.comp_r[rg * 4 + i] != cc;
                             const uint64_t bv = (uint64_t)__double_as_longlong(acc[i][j]);
-                            if (ok) tie_merge_bits(m, mj, bv, (int32_t)(gr0 + i));
+                            if (ok && bv < m) { m = bv; mj = (int32_t)(gr0 + i); }
+                            else if (ok && bv == m) mj |= TIEBIT;
                         }
 #pragma unroll
                         for (int off = 8; off < 32; off <<= 1) {

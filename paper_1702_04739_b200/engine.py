@@ -328,6 +328,15 @@ class CudaBackend:
         check(self.lib.isoc_prim_edges(_ptr(X), n, d, root, _ptr(u), _ptr(v), _ptr(w), self.stream))
         return u, v, w
 
+    def mst_filter_stats(self, h):
+        """(256-row blocks scanned by the tc filter, blocks x filter rounds,
+        rows whose candidate list ran out)."""
+        if not hasattr(self.lib, "isoc_mst_filter_stats"):   # an older variant build (ISOC_LIB_PATH)
+            return None
+        run, tot, rows = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(self.lib.isoc_mst_filter_stats(h, ctypes.byref(run), ctypes.byref(tot), ctypes.byref(rows)))
+        return run.value, tot.value, rows.value
+
     def mst_destroy(self, h) -> None:
         self.lib.isoc_mst_destroy(h)
 

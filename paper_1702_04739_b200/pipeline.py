@@ -233,6 +233,9 @@ def _boruvka(P: _Points, nn=None, sigma: Optional[float] = None) -> tuple:
         while comps > 1:
             comps = _progress(one_round(None), comps, stats)
         u, v, w = b.mst_edges(h, n)
+        fs = getattr(b, "mst_filter_stats", lambda _h: None)(h)
+        if fs is not None:
+            stats["filter_blocks_run"], stats["filter_blocks_total"], stats["filter_rows_refreshed"] = fs
     finally:
         b.mst_destroy(h)
     if comm.world > 1:
