@@ -576,7 +576,11 @@ int isoc_omega_mst(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi
     cudaMemGetInfo(&free_b, &total_b);
     const double ps_bytes = (double)nbs * (double)n * (comp ? 20.0 : 8.0);
     const bool sym_fits = ps_bytes < 0.6 * (double)free_b;
-    if (lo == 0 && hi == n && sym_fits && getenv("ISOC_OMEGA_ROWS") == nullptr) {
+    // the symmetric pass once its I <= J super-tiles fill the SMs (n >~ 17k);
+    // below that the row pass finishes sooner (bitwise identical)
+    const int mode = passes_mode();
+    const bool sym_wide = mode == 1 || (mode == 0 && nbs * (nbs + 1) / 2 >= device_sm_count());
+    if (lo == 0 && hi == n && sym_fits && sym_wide) {
         CK(launch_omega_sym(X, n, d, sigma, comp, omega, nn_j, nn_d, nn_tie, (cudaStream_t)stream));
     } else {
         CK(launch_omega_pass(X, n, d, lo, hi, sigma, comp, omega, nn_j, nn_d, nn_tie,

@@ -603,6 +603,168 @@ __global__ void __launch_bounds__(512, 2) decide_multi_kernel(DecideBatchArgs A)
     }
 }
 
+// ---------------------------------------------------- small trees (C1)
+// A tree whose per-vertex state fits in one CTA's shared memory (n of a few
+// thousand, e.g. the MST of config C1 with 228 levels) is swept by ONE CTA per
+// threshold with every array staged in shared memory: a level costs a few
+// __syncthreads and shared-memory latencies instead of two grid barriers and
+// dependent global loads.  Same arithmetic, canonical order, k-th-cut stop
+// and fold order as decide_kernel (which is this with G = 1).
+constexpr int DS_THREADS = 32;
+
+size_t decide_small_smem(int64_t n, int64_t levels) {
+    // f, om0, p0, om, p (8 B) + child_lo, child_cnt, excl (4 B) + code (1 B) + level_off
+    return (size_t)n * (5 * 8 + 3 * 4 + 1) + (size_t)(levels + 1) * 8 + 64;
+}
+
+struct DecideSmallArgs {
+    int64_t n;
+    int64_t levels;
+    const int64_t* level_off;
+    const double* f_pos;
+    const double* om0;
+    const double* p0;
+    const int32_t* child_lo;
+    const int32_t* child_cnt;
+    const double* thr;   // K thresholds (device) -- one CTA each
+    int64_t k;
+    int8_t* code;        // witness (K == 1): per-position codes, else nullptr
+    double* spars;       // witness: k sparsities in cut order, else nullptr
+    int64_t* j_out;      // [K]
+};
+
+__global__ void __launch_bounds__(DS_THREADS, 1) decide_small_kernel(DecideSmallArgs A) {
+    // one warp per threshold: MST levels are narrow (median width 6-71 at
+    // C1), so a level is a few shuffles and __syncwarp()s
+    extern __shared__ __align__(16) unsigned char ds_raw[];
+    const int lane = threadIdx.x;
+    const int64_t n = A.n, L = A.levels;
+    double* f = reinterpret_cast<double*>(ds_raw);
+    double* om0 = f + n;
+    double* p0 = om0 + n;
+    double* om = p0 + n;
+    double* pp = om + n;
+    int64_t* loff = reinterpret_cast<int64_t*>(pp + n);
+    int32_t* clo = reinterpret_cast<int32_t*>(loff + L + 1);
+    int32_t* ccnt = clo + n;
+    int32_t* excl = ccnt + n;
+    int8_t* code = reinterpret_cast<int8_t*>(excl + n);
+    for (int64_t q = lane; q < n; q += 32) {
+        f[q] = A.f_pos[q];
+        om0[q] = A.om0[q];
+        p0[q] = A.p0[q];
+        clo[q] = A.child_lo[q];
+        ccnt[q] = A.child_cnt[q];
+        code[q] = 0;
+    }
+    for (int64_t q = lane; q <= L; q += 32) loff[q] = A.level_off[q];
+    __syncwarp();
+    const double thr = A.thr[blockIdx.x];
+    const bool witness = A.code != nullptr;
+    int64_t j = 0, stop_lo = 0;
+    for (int64_t lv = L - 1; lv >= 0; --lv) {
+        const int64_t lo = loff[lv], hi = loff[lv + 1];
+        const bool deepest = lv == L - 1;
+        const double* pv = deepest ? p0 : pp;
+        const double* ov = deepest ? om0 : om;
+        const int64_t W = hi - lo;
+        // conditions and the exclusive cut prefix in canonical (descending
+        // position) order over the whole level
+        int32_t carry = 0;
+        for (int64_t base = 0; base < W; base += 32) {
+            const int64_t c = base + lane;
+            int32_t is_cut = 0;
+            if (c < W) {
+                const int64_t pos = hi - 1 - c;
+                const double rhs = __dmul_rn(thr, ov[pos]);
+                int8_t cond;
+                if (__dadd_rn(f[pos], pv[pos]) <= rhs) cond = 1;
+                else if (__dsub_rn(pv[pos], f[pos]) < rhs) cond = 2;
+                else cond = 3;
+                code[pos] = cond;
+                is_cut = cond == 1;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, is_cut);
+            if (c < W) excl[hi - 1 - c] = carry + __popc(bal & ((1u << lane) - 1u));
+            carry += __popc(bal);
+        }
+        __syncwarp();
+        const int64_t need = A.k - j;
+        const int64_t tot = carry;
+        if (lv > 0) {
+            // one lane per parent folds its children in descending child
+            // rank, committing each (fewer than need cuts precede it)
+            const int64_t plo = loff[lv - 1];
+            for (int64_t u = plo + lane; u < lo; u += 32) {
+                const int32_t c0 = clo[u], cn = ccnt[u];
+                double pu = p0[u], ou = om0[u];
+                for (int32_t q = c0 + cn - 1; q >= c0; --q) {
+                    int8_t d = code[q];
+                    const int64_t e = excl[q];
+                    if (e < need) {
+                        if (d == 1 && witness) A.spars[j + e] = __ddiv_rn(__dadd_rn(f[q], pv[q]), ov[q]);
+                    } else {
+                        code[q] = 0;
+                        d = 0;
+                    }
+                    if (d == 1 || d == 3) {
+                        pu = __dadd_rn(pu, f[q]);
+                    } else if (d == 2) {
+                        ou = __dadd_rn(ou, ov[q]);
+                        pu = __dadd_rn(pu, pv[q]);
+                    }
+                }
+                pp[u] = pu;
+                om[u] = ou;
+            }
+        } else {
+            for (int64_t c = lane; c < W; c += 32) {
+                const int64_t pos = hi - 1 - c;
+                const int64_t e = excl[pos];
+                if (e < need) {
+                    if (code[pos] == 1 && witness) A.spars[j + e] = __ddiv_rn(__dadd_rn(f[pos], pv[pos]), ov[pos]);
+                } else {
+                    code[pos] = 0;
+                }
+            }
+        }
+        j += (tot < need) ? tot : need;
+        __syncwarp();
+        if (j >= A.k) { stop_lo = lo; break; }
+    }
+    if (witness) {
+        for (int64_t q = lane; q < n; q += 32) A.code[q] = q < stop_lo ? 0 : code[q];
+    }
+    if (lane == 0) A.j_out[blockIdx.x] = j;
+}
+
+static bool decide_small_fits(int64_t n, int64_t levels, size_t* smem) {
+    *smem = decide_small_smem(n, levels);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return *smem <= (size_t)optin;
+}
+
+static cudaError_t launch_decide_small(int64_t n, int64_t levels, const int64_t* level_off, const double* f_pos,
+                                       const double* om0, const double* p0, const int32_t* child_lo,
+                                       const int32_t* child_cnt, const double* thr, int K, int64_t k,
+                                       int8_t* code, double* spars, int64_t* j_out, size_t smem,
+                                       cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(decide_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    DecideSmallArgs A;
+    A.n = n; A.levels = levels; A.level_off = level_off; A.f_pos = f_pos; A.om0 = om0; A.p0 = p0;
+    A.child_lo = child_lo; A.child_cnt = child_cnt; A.thr = thr; A.k = k; A.code = code; A.spars = spars;
+    A.j_out = j_out;
+    const int pid = prof_begin(PK_DECIDE, st);
+    decide_small_kernel<<<K, DS_THREADS, smem, st>>>(A);
+    prof_end(pid, st);
+    note_launch();
+    return cudaGetLastError();
+}
+
 int decide_grid_size(int64_t max_width);
 
 cudaError_t launch_decide_batch(int64_t n, int64_t levels, const int64_t* level_off, int64_t max_width,
@@ -610,6 +772,10 @@ cudaError_t launch_decide_batch(int64_t n, int64_t levels, const int64_t* level_
                                 const int32_t* child_lo, const int32_t* child_cnt, const double* thr,
                                 int K, int64_t k, double* om, double* p, int8_t* code, int32_t* excl,
                                 int32_t* scratch, int64_t* j_out, cudaStream_t st) {
+    size_t smem = 0;
+    if (decide_small_fits(n, levels, &smem))
+        return launch_decide_small(n, levels, level_off, f_pos, om0, p0, child_lo, child_cnt, thr, K, k,
+                                   nullptr, nullptr, j_out, smem, st);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -675,6 +841,14 @@ cudaError_t launch_decide(int64_t n, int64_t levels, const int64_t* level_off, i
                           const int32_t* child_lo, const int32_t* child_cnt, double thr, int64_t k,
                           double* om, double* p, int8_t* code, int32_t* excl, double* spars,
                           int32_t* scratch, int64_t* j_out, cudaStream_t st) {
+    size_t smem = 0;
+    if (decide_small_fits(n, levels, &smem)) {
+        // the threshold goes to the device through the scratch tail
+        double* dthr = reinterpret_cast<double*>(scratch + 1024 + 16);
+        cudaMemcpyAsync(dthr, &thr, sizeof(double), cudaMemcpyHostToDevice, st);
+        return launch_decide_small(n, levels, level_off, f_pos, om0, p0, child_lo, child_cnt, dthr, 1, k, code,
+                                   spars, j_out, smem, st);
+    }
     const int G = decide_grid_size(max_width);
     DecideArgs A;
     A.n = n; A.levels = levels; A.level_off = level_off; A.f_pos = f_pos; A.om0 = om0; A.p0 = p0;

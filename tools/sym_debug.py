@@ -8,8 +8,7 @@ for n, d in [(2048, 3), (2049, 5), (3000, 16), (4099, 9), (4099, 16), (4099, 8),
     pts, _ = orc.generate_random(n, d, 4, 1)
     out = {}
     for mode in ("sym", "rows"):
-        if mode == "rows": os.environ["ISOC_SIGMA_ROWS"] = "1"
-        else: os.environ.pop("ISOC_SIGMA_ROWS", None)
+        os.environ["ISOC_PASSES"] = mode
         P = pipeline._Points(pts)
         stack, (nj, nd, nt), _ = pipeline._sigma_pass(P, 0.0)
         try:
