@@ -13,6 +13,7 @@
 #include "../../include/isoclust_b200.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "scratch.h"
 
 using namespace isoc;
 
@@ -713,24 +714,25 @@ int isoc_tree_from_edges(const int32_t* u, const int32_t* v, const double* w, in
     int32_t *off = nullptr, *adj = nullptr, *work = nullptr;
     double* adjd = nullptr;
     int64_t* lv = nullptr;
+    int64_t levels = 0;
     cudaStream_t st = t->st;
 #define TCK(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { cudaGetLastError(); tree_free(t); \
     return fail(_e == cudaErrorMemoryAllocation ? ISOC_ENOMEM : ISOC_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e)); } } while (0)
-    TCK(aalloc(&off, n + 1, st));
-    TCK(aalloc(&adj, 2 * n, st));
-    TCK(aalloc(&adjd, 2 * n, st));
-    TCK(aalloc(&work, n + 2, st));
-    TCK(aalloc(&lv, 1, st));
+    {
+    Scratch sc(st);   // off / adj / adjd / work / lv freed on every return path
+    TCK(sc.alloc(&off, n + 1));
+    TCK(sc.alloc(&adj, 2 * n));
+    TCK(sc.alloc(&adjd, 2 * n));
+    TCK(sc.alloc(&work, n + 2));
+    TCK(sc.alloc(&lv, 1));
     TCK(launch_build_adjacency(u, v, w, n, off, adj, adjd, work, st));
     TCK(launch_bfs(n, root, 1, off, adj, adjd, t->bfs, t->pos_of, t->parent_v, t->depth_v,
                    t->child_id_v, t->parent_d, t->pos_parent, t->child_lo, t->child_cnt, t->level_off,
                    t->scratch, lv, st));
     TCK(launch_flows(t->parent_d, t->parent_v, n, sigma, t->flow_v, st));
-    int64_t levels = 0;
     TCK(cudaMemcpyAsync(&levels, lv, sizeof levels, cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(off, st); cudaFreeAsync(adj, st); cudaFreeAsync(adjd, st);
-    cudaFreeAsync(work, st); cudaFreeAsync(lv, st);
     TCK(cudaStreamSynchronize(st));
+    }
     rc = tree_finish_layout(t, levels);
     if (rc) { tree_free(t); return rc; }
     *out = t;
@@ -750,10 +752,13 @@ int isoc_tree_from_parent(const int64_t* parent, const double* flow, const int64
     cudaStream_t st = t->st;
     int32_t *off = nullptr, *adj = nullptr, *flags = nullptr;
     int64_t* lv = nullptr;
-    TCK(aalloc(&off, n + 1, st));
-    TCK(aalloc(&adj, n, st));
-    TCK(aalloc(&flags, 3, st));
-    TCK(aalloc(&lv, 1, st));
+    int64_t levels = 0;
+    {
+    Scratch sc(st);   // off / adj / flags / lv freed on every return path
+    TCK(sc.alloc(&off, n + 1));
+    TCK(sc.alloc(&adj, n));
+    TCK(sc.alloc(&flags, 3));
+    TCK(sc.alloc(&lv, 1));
     TCK(cudaMemsetAsync(flags, 0, 2 * sizeof(int32_t), st));
     TCK(cudaMemsetAsync(flags + 2, 0xff, sizeof(int32_t), st));   // found root: -1
     TCK(launch_children_from_parent(parent, child_id, n, root, off, adj, t->child_id_v, flags,
@@ -776,11 +781,9 @@ int isoc_tree_from_parent(const int64_t* parent, const double* flow, const int64
                    t->scratch, lv, st));
     TCK(cudaMemcpyAsync(t->flow_v, flow, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
     root_flow_kernel<<<1, 1, 0, st>>>(t->flow_v, root);
-    int64_t levels = 0;
     TCK(cudaMemcpyAsync(&levels, lv, sizeof levels, cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(off, st); cudaFreeAsync(adj, st);
-    cudaFreeAsync(flags, st); cudaFreeAsync(lv, st);
     TCK(cudaStreamSynchronize(st));
+    }
     rc = tree_finish_layout(t, levels);
     if (rc) { tree_free(t); return rc; }
     *out = t;

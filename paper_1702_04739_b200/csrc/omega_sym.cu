@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "scratch.h"
 #include "kernels.h"
 #include "prof.h"
 
@@ -530,8 +531,9 @@ static cudaError_t omega_sym_tiles(const double* X, int64_t n, int d, double sig
     const int64_t nbs = (n + SB - 1) / SB;
     const int64_t np = nbs * SB;
     const int dpad = (d + SK - 1) / SK * SK;
+    Scratch sc(st);
     double* XT = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&XT, (size_t)np * dpad * 8, st);
+    cudaError_t e = sc.alloc(&XT, (size_t)np * dpad);
     if (e != cudaSuccess) return e;
     e = launch_transpose_pad(X, n, d, np, dpad, XT, st);
     if (e != cudaSuccess) return e;
@@ -547,7 +549,6 @@ static cudaError_t omega_sym_tiles(const double* X, int64_t n, int d, double sig
         prof_end(pid, st);
         note_launch(1);
     }
-    cudaFreeAsync(XT, st);
     return cudaGetLastError();
 }
 
@@ -555,14 +556,15 @@ cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, co
                              double* omega, int32_t* nn_j, double* nn_d, int8_t* nn_tie,
                              cudaStream_t st) {
     const int64_t nbs = (n + SB - 1) / SB;
+    Scratch sc(st);   // PS / PSm / PSj freed on every return path
     double *PS = nullptr, *PSm = nullptr;
     int32_t* PSj = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&PS, (size_t)nbs * n * 8, st);
+    cudaError_t e = sc.alloc(&PS, (size_t)nbs * n);
     if (e != cudaSuccess) return e;
     if (comp) {
-        e = cudaMallocAsync((void**)&PSm, (size_t)nbs * n * 8, st);
+        e = sc.alloc(&PSm, (size_t)nbs * n);
         if (e != cudaSuccess) return e;
-        e = cudaMallocAsync((void**)&PSj, (size_t)nbs * n * 4, st);
+        e = sc.alloc(&PSj, (size_t)nbs * n);
         if (e != cudaSuccess) return e;
     }
     e = omega_sym_tiles(X, n, d, sigma, comp, 0, nbs, 1, n, PS, PSm, PSj, st);
@@ -570,9 +572,6 @@ cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, co
     omega_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(PS, PSm, PSj, n, nbs, 1, n, omega, nn_j,
                                                                      nn_d, nn_tie);
     note_launch(1);
-    cudaFreeAsync(PS, st);
-    if (PSm) cudaFreeAsync(PSm, st);
-    if (PSj) cudaFreeAsync(PSj, st);
     return cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@
 
 #include "../../include/isoclust_b200.h"
 #include "common.cuh"
+#include "scratch.h"
 #include "kernels.h"
 #include "leaf.h"
 #include "prof.h"
@@ -284,23 +285,6 @@ __global__ void __launch_bounds__(256) brute_force_kernel(const int32_t* __restr
 }
 
 inline unsigned nb(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
-
-// Stream-ordered scratch freed on every return path.
-struct Scratch {
-    cudaStream_t st;
-    void* ptrs[16];
-    int count = 0;
-    explicit Scratch(cudaStream_t s) : st(s) {}
-    template <typename T>
-    cudaError_t alloc(T** p, size_t elems) {
-        cudaError_t e = cudaMallocAsync((void**)p, (elems ? elems : 1) * sizeof(T), st);
-        if (e == cudaSuccess && count < 16) ptrs[count++] = *p;
-        return e;
-    }
-    ~Scratch() {
-        for (int i = 0; i < count; ++i) cudaFreeAsync(ptrs[i], st);
-    }
-};
 
 }  // namespace
 }  // namespace isoc
