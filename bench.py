@@ -555,8 +555,14 @@ def main():
     alg = {
         "sigma_pass": 3.0 * d * unordered,
         "omega_pass": 3.0 * d * unordered,
-        # tcgen05 filter: 3 FP16 MMA passes (hi.hi, hi.lo, lo.hi) over K = 64 per atom per pair
-        "boruvka_filter": (3 * 2.0 * 64 * ((d + 63) // 64) if use_tc else 2.0 * d) * n * n,
+        # tcgen05 filter: 3 FP16 MMA passes (hi.hi, hi.lo, lo.hi) over K = 64 per atom per
+        # (row, column) pair it scans; with the candidate lists later launches scan only
+        # the refreshed rows, so the per-launch figure is the step's rows scanned x n
+        # spread over its launches (the kernel line below divides by launches)
+        "boruvka_filter": (3 * 2.0 * 64 * ((d + 63) // 64) if use_tc else 2.0 * d) * n *
+                          (256.0 * run.mst_stats.get("filter_blocks_run", 0)
+                           / max(1.0, kernels.get("boruvka_filter", {}).get("launches", 1.0))
+                           if use_tc and run.mst_stats.get("filter_blocks_run") else n),
     }
     # the exact passes' fp64 ops cannot fuse (scipy's separately rounded
     # mul/add), so their ceiling is the DADD/DMUL issue rate = half the
@@ -609,7 +615,7 @@ def main():
         # DRAM bytes per launch of the dominant kernel from the committed ncu
         # launch list of the same configuration (bench.py cannot run ncu itself)
         try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_c3.json")))
+            tr = json.load(open(os.path.join(ROOT, "profiles", "round2_traffic_c3.json")))
             if tr.get("config") == f"c3 N={n} d={d} k={k}" and dom in tr:
                 roofline["traffic"] = tr[dom]
                 roofline["traffic_unit"] = "bytes per launch"
@@ -640,10 +646,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # bounded sample (~10-30 s of host work): the oracle port of the whole
-        # reference pipeline at N=16,000 (or the workload itself when smaller),
-        # per phase, extrapolated with the N^2 / N phase model
+        # reference pipeline on the ladder N = 16,000 / 32,000 / 46,340 (or the
+        # workload itself when smaller), per phase, extrapolated with the
+        # N^2 / N phase model -- the same measurement as --impl reference
         threads = os.cpu_count() or 1
-        ref = cpu_reference(n, d, k, (16_000,), 1, threads, 0)
+        ref = cpu_reference(n, d, k, LADDER, 1, threads, 0)
         cpu = {"value": n / ref["seconds"], "unit": "points/s", "cores": threads, "kind": "port",
                "sample": ref["sample"], **{kk: v for kk, v in ref.items() if kk in ("ladder", "fit", "phases_s")}}
 
