@@ -68,9 +68,9 @@ SIGNATURES = {
     "isoc_sigma_rank_merge": (ctypes.c_int, [P, I64, I32, I64, I64, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "isoc_omega": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P]),
     "isoc_omega_mst": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, P, P, P, P, P]),
-    "isoc_omega_shard_shape": (ctypes.c_int, [I64, I32, PI64, PI64]),
-    "isoc_omega_sym_range": (ctypes.c_int, [P, I64, I32, I64, I64, D, P, I32, P, P, P, P]),
-    "isoc_omega_rank_merge": (ctypes.c_int, [I64, I64, I64, I32, P, P, P, P, P, P, P, P]),
+    "isoc_omega_shard_counts": (ctypes.c_int, [I64, I32, I32, P, P]),
+    "isoc_omega_sym_range": (ctypes.c_int, [P, I64, I32, I32, I32, D, P, P, P, P, P]),
+    "isoc_omega_rank_merge": (ctypes.c_int, [I64, I32, I32, P, P, P, P, P, P, P, P]),
     "isoc_distance_matrix": (ctypes.c_int, [P, I64, I32, P, P]),
     "isoc_flow": (ctypes.c_int, [P, I64, D, P, P]),
     "isoc_vertex_weights_dense": (ctypes.c_int, [P, I64, D, P, P]),

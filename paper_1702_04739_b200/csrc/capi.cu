@@ -590,38 +590,32 @@ int isoc_omega_mst(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi
     return ISOC_OK;
 }
 
-int isoc_omega_shard_shape(int64_t n, int32_t G, int64_t* nbs, int64_t* rows_pad) {
-    if (n < 2 || G < 1) return fail(ISOC_EINVAL, "need n >= 2 and G >= 1");
-    omega_sym_shard_shape(n, G, nbs, rows_pad);
+int isoc_omega_shard_counts(int64_t n, int32_t G, int32_t rank, int64_t* send_counts, int64_t* recv_counts) {
+    if (n < 2 || G < 1 || rank < 0 || rank >= G) return fail(ISOC_EINVAL, "need n >= 2 and 0 <= rank < G");
+    if (!send_counts || !recv_counts) return fail(ISOC_EINVAL, "missing count arrays");
+    omega_shard_counts(n, G, rank, send_counts, recv_counts);
     return ISOC_OK;
 }
 
-int isoc_omega_sym_range(const double* X, int64_t n, int32_t d, int64_t jlo, int64_t jhi, double sigma,
-                         isoc_mst* h, int32_t G, double* ps, double* psm, int32_t* psj, void* stream) {
+int isoc_omega_sym_range(const double* X, int64_t n, int32_t d, int32_t rank, int32_t G, double sigma,
+                         isoc_mst* h, double* ps, double* psm, int32_t* psj, void* stream) {
     if (n < 2 || d < 1) return fail(ISOC_EINVAL, "need n >= 2 and d >= 1");
     if (n > (int64_t)INT32_MAX) return fail(ISOC_EINVAL, "n too large");
     if (!(sigma > 0.0)) return fail(ISOC_EINVAL, "sigma must be > 0, got %g", sigma);
-    if (G < 1) return fail(ISOC_EINVAL, "need at least one rank");
-    const int64_t nbs = (n + 1023) / 1024;
-    if (jlo < 0 || jhi > nbs || jlo > jhi)
-        return fail(ISOC_EINVAL, "bad block range [%lld, %lld)", (long long)jlo, (long long)jhi);
+    if (G < 1 || rank < 0 || rank >= G) return fail(ISOC_EINVAL, "need 0 <= rank < G");
     if (!ps || (h && (!psm || !psj))) return fail(ISOC_EINVAL, "missing slot buffers");
     ensure_pool();
-    CK(launch_omega_sym_range(X, n, d, sigma, h ? h->comp : nullptr, jlo, jhi, G, ps, psm, psj,
+    CK(launch_omega_sym_range(X, n, d, sigma, h ? h->comp : nullptr, rank, G, ps, psm, psj,
                               (cudaStream_t)stream));
     return ISOC_OK;
 }
 
-int isoc_omega_rank_merge(int64_t n, int64_t lo, int64_t hi, int32_t G, const double* ps, const double* psm,
+int isoc_omega_rank_merge(int64_t n, int32_t rank, int32_t G, const double* ps, const double* psm,
                           const int32_t* psj, double* omega, int32_t* nn_j, double* nn_d, int8_t* nn_tie,
                           void* stream) {
-    if (n < 2 || G < 1) return fail(ISOC_EINVAL, "need n >= 2 and G >= 1");
-    if (lo < 0 || hi > n || lo >= hi) return fail(ISOC_EINVAL, "bad row range");
-    int64_t nbs, rows_pad;
-    omega_sym_shard_shape(n, G, &nbs, &rows_pad);
-    if (hi - lo > rows_pad) return fail(ISOC_EINVAL, "row range wider than a shard");
+    if (n < 2 || G < 1 || rank < 0 || rank >= G) return fail(ISOC_EINVAL, "need n >= 2 and 0 <= rank < G");
     if (psm && (!psj || !nn_j || !nn_d || !nn_tie)) return fail(ISOC_EINVAL, "missing neighbour buffers");
-    CK(launch_omega_rank_merge(n, lo, hi, G, ps, psm, psj, omega, nn_j, nn_d, nn_tie, (cudaStream_t)stream));
+    CK(launch_omega_rank_merge(n, rank, G, ps, psm, psj, omega, nn_j, nn_d, nn_tie, (cudaStream_t)stream));
     return ISOC_OK;
 }
 

@@ -61,9 +61,6 @@ constexpr int DK_MAXG = 1024;  // chunk counts live in scratch[0, 1024)
 #ifndef DK_FOLD_COND
 #define DK_FOLD_COND 0  // 1: load a child's f / omega / p only where its condition uses them
 #endif
-#ifndef DK_MULTI
-#define DK_MULTI 1      // wide trees: batched thresholds share the CTAs (decide_multi_kernel)
-#endif
 #ifndef DK_MINB
 #define DK_MINB 2 // resident CTAs per SM the register budget is sized for
 #endif
@@ -449,160 +446,6 @@ __global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
     if (bi == 0 && tid == 0) A.j_out[kk] = j;
 }
 
-// Fused batch for wide trees: all KM thresholds on the same CTAs, one
-// element / parent per thread for every threshold, so a vertex's flow,
-// child range and parent weights are loaded once per sweep instead of once
-// per threshold, and the level latency (grid barriers, dependent child
-// loads) is paid once for KM bisection candidates.  Per threshold the
-// arithmetic, commit rule and fold order are decide_kernel's.
-template <int KM>
-__global__ void __launch_bounds__(512, 2) decide_multi_kernel(DecideBatchArgs A) {
-    __shared__ int32_t warp_tot[16];
-    __shared__ int32_t s_pre[KM][DK_MAXG + 1];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    const int bd = blockDim.x;
-    const int G = gridDim.x, b = blockIdx.x;
-    const int64_t n = A.n;
-    double thr[KM];
-    int64_t j[KM];
-#pragma unroll
-    for (int t = 0; t < KM; ++t) {
-        thr[t] = A.thr[t];
-        j[t] = 0;
-    }
-    for (int64_t lv = A.levels - 1; lv >= 0; --lv) {
-        const int64_t lo = A.level_off[lv], hi = A.level_off[lv + 1];
-        const bool deepest = lv == A.levels - 1;
-        bool act[KM];
-#pragma unroll
-        for (int t = 0; t < KM; ++t) act[t] = j[t] < A.k;
-        const uint32_t W = (uint32_t)(hi - lo);
-        const uint32_t CH = (W + G - 1) / G;
-        const uint32_t cb = min(W, (uint32_t)b * CH), ce = min(W, cb + CH);
-        int32_t carry[KM];
-#pragma unroll
-        for (int t = 0; t < KM; ++t) carry[t] = 0;
-        for (uint32_t base = cb; base < ce; base += bd) {
-            const uint32_t c = base + tid;
-            const bool in = c < ce;
-            const int64_t pos = hi - 1 - (int64_t)c;
-            // KM 16-bit cut counts packed in one word for the block scan (<= 512 each)
-            uint64_t packed = 0;
-            if (in) {
-                const double f = A.f_pos[pos];
-#pragma unroll
-                for (int t = 0; t < KM; ++t)
-                    if (act[t]) {
-                        const double pw = deepest ? A.p0[pos] : A.p[t * n + pos];
-                        const double ow = deepest ? A.om0[pos] : A.om[t * n + pos];
-                        const double rhs = __dmul_rn(thr[t], ow);
-                        int8_t cond;
-                        if (__dadd_rn(f, pw) <= rhs) cond = 1;
-                        else if (__dsub_rn(pw, f) < rhs) cond = 2;
-                        else cond = 3;
-                        A.code[t * n + pos] = cond;
-                        if (cond == 1) packed |= (uint64_t)1 << (16 * t);
-                    }
-            }
-            const uint64_t mine = packed;
-            uint64_t x = packed;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            __shared__ uint64_t wtot[16];
-            if (lane == 31) wtot[wid] = x;
-            __syncthreads();
-            if (wid == 0) {
-                uint64_t tt = lane < nw ? wtot[lane] : 0;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint64_t y = __shfl_up_sync(0xffffffffu, tt, o);
-                    if (lane >= o) tt += y;
-                }
-                if (lane < nw) wtot[lane] = tt;
-            }
-            __syncthreads();
-            const uint64_t ex = (wid > 0 ? wtot[wid - 1] : 0) + x - mine;
-            const uint64_t blk = wtot[nw - 1];
-#pragma unroll
-            for (int t = 0; t < KM; ++t) {
-                if (in && act[t]) A.excl[t * n + pos] = carry[t] + (int32_t)((ex >> (16 * t)) & 0xffff);
-                carry[t] += (int32_t)((blk >> (16 * t)) & 0xffff);
-            }
-            __syncthreads();
-        }
-        if (tid == 0) {
-#pragma unroll
-            for (int t = 0; t < KM; ++t) A.chunk_cnt[t * DK_MAXG + b] = carry[t];
-        }
-        grid_barrier(A.bar);
-#pragma unroll
-        for (int t = 0; t < KM; ++t) chunk_prefix(A.chunk_cnt + t * DK_MAXG, G, s_pre[t], warp_tot);
-        int64_t need[KM], tot[KM];
-#pragma unroll
-        for (int t = 0; t < KM; ++t) {
-            need[t] = A.k - j[t];
-            tot[t] = s_pre[t][G];
-        }
-        if (lv > 0) {
-            const int64_t plo = A.level_off[lv - 1];
-            const int64_t PW = lo - plo;
-            const int64_t ub = plo + (PW * b) / G, ue = plo + (PW * (b + 1)) / G;
-            for (int64_t u = ub + tid; u < ue; u += bd) {
-                const int32_t clo = A.child_lo[u], cnt = A.child_cnt[u];
-                const double p0u = A.p0[u], o0u = A.om0[u];
-                double pu[KM], ou[KM];
-#pragma unroll
-                for (int t = 0; t < KM; ++t) {
-                    pu[t] = p0u;
-                    ou[t] = o0u;
-                }
-                for (int32_t q = clo + cnt - 1; q >= clo; --q) {
-                    const double fq = A.f_pos[q];
-                    const uint32_t c = (uint32_t)(hi - 1 - q);
-                    const uint32_t cq = c / CH;
-#pragma unroll
-                    for (int t = 0; t < KM; ++t) {
-                        if (!act[t]) continue;
-                        int8_t d = A.code[t * n + q];
-                        const int64_t e = (int64_t)s_pre[t][cq] + A.excl[t * n + q];
-                        if (e >= need[t]) {
-                            A.code[t * n + q] = 0;
-                            d = 0;
-                        }
-                        if (d == 1 || d == 3) {
-                            pu[t] = __dadd_rn(pu[t], fq);
-                        } else if (d == 2) {
-                            const double oq = deepest ? A.om0[q] : A.om[t * n + q];
-                            const double pq = deepest ? A.p0[q] : A.p[t * n + q];
-                            ou[t] = __dadd_rn(ou[t], oq);
-                            pu[t] = __dadd_rn(pu[t], pq);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int t = 0; t < KM; ++t)
-                    if (act[t]) {
-                        A.p[t * n + u] = pu[t];
-                        A.om[t * n + u] = ou[t];
-                    }
-            }
-        }
-        bool all_done = true;
-#pragma unroll
-        for (int t = 0; t < KM; ++t) {
-            if (act[t]) j[t] += (tot[t] < need[t]) ? tot[t] : need[t];
-            all_done &= j[t] >= A.k;
-        }
-        grid_barrier(A.bar);
-        if (all_done) break;
-    }
-    if (b == 0 && tid == 0) {
-#pragma unroll
-        for (int t = 0; t < KM; ++t) A.j_out[t] = j[t];
-    }
-}
-
 // ---------------------------------------------------- small trees (C1)
 // A tree whose per-vertex state fits in one CTA's shared memory (n of a few
 // thousand, e.g. the MST of config C1 with 228 levels) is swept by ONE CTA per
@@ -783,30 +626,6 @@ cudaError_t launch_decide_batch(int64_t n, int64_t levels, const int64_t* level_
     const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     int64_t gi = (max_width + 8191) / 8192;
     if (gi < 1) gi = 1;
-    // ISOC_DECIDE_MULTI=1 forces the fused kernel (tests), =0 disables it
-    const char* fm = getenv("ISOC_DECIDE_MULTI");
-    const int force_multi = fm ? atoi(fm) : -1;
-    const bool wide = force_multi < 0 ? (gi * K > cap && DK_MULTI) : force_multi > 0;
-    if (K >= 2 && K <= 3 && wide) {
-        // wide tree: the instances would split the CTAs a single sweep wants,
-        // so they share them instead (decide_multi_kernel)
-        const int Gm = decide_grid_size(max_width);
-        DecideBatchArgs A;
-        A.n = n; A.levels = levels; A.level_off = level_off; A.f_pos = f_pos; A.om0 = om0; A.p0 = p0;
-        A.child_lo = child_lo; A.child_cnt = child_cnt; A.thr = thr; A.K = K; A.k = k; A.om = om; A.p = p;
-        A.code = code; A.excl = excl; A.chunk_cnt = scratch; A.j_out = j_out;
-        A.bar = reinterpret_cast<unsigned int*>(scratch + DB_MAX * 1024);
-        cudaMemsetAsync(A.bar, 0, 2 * sizeof(unsigned int), st);
-        void* args[] = {&A};
-        const int pid = prof_begin(PK_DECIDE, st);
-        cudaError_t e = K == 2 ? cudaLaunchCooperativeKernel((void*)decide_multi_kernel<2>, dim3(Gm), dim3(512),
-                                                             args, 0, st)
-                               : cudaLaunchCooperativeKernel((void*)decide_multi_kernel<3>, dim3(Gm), dim3(512),
-                                                             args, 0, st);
-        prof_end(pid, st);
-        note_launch();
-        return e;
-    }
     if (gi * K > cap) gi = cap / K > 0 ? cap / K : 1;
     const int G = (int)(gi * K);
     DecideBatchArgs A;

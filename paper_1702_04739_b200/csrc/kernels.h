@@ -52,13 +52,15 @@ void sym_block_range(int64_t n, int rank, int world, int64_t* jlo, int64_t* jhi,
 cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, const int32_t* comp,
                              double* omega, int32_t* nn_j, double* nn_d, int8_t* nn_tie,
                              cudaStream_t st);
-void omega_sym_shard_shape(int64_t n, int G, int64_t* nbs, int64_t* rows_pad);
+// sharded symmetric omega: per-peer slot counts of rank `rank` (send[g] to
+// owner g, recv[s] from sender s); the send / receive buffers are the
+// concatenations of the messages in peer order
+void omega_shard_counts(int64_t n, int G, int rank, int64_t* send, int64_t* recv);
 cudaError_t launch_omega_sym_range(const double* X, int64_t n, int d, double sigma, const int32_t* comp,
-                                   int64_t jlo, int64_t jhi, int G, double* PS, double* PSm, int32_t* PSj,
-                                   cudaStream_t st);
-cudaError_t launch_omega_rank_merge(int64_t n, int64_t lo, int64_t hi, int G, const double* PS,
-                                    const double* PSm, const int32_t* PSj, double* omega, int32_t* nn_j,
-                                    double* nn_d, int8_t* nn_tie, cudaStream_t st);
+                                   int rank, int G, double* PS, double* PSm, int32_t* PSj, cudaStream_t st);
+cudaError_t launch_omega_rank_merge(int64_t n, int rank, int G, const double* PS, const double* PSm,
+                                    const int32_t* PSj, double* omega, int32_t* nn_j, double* nn_d,
+                                    int8_t* nn_tie, cudaStream_t st);
 
 // boruvka.cu
 cudaError_t launch_prep_fp32(const double* X, int64_t n, int d, int dp, int64_t npad, double* centre,

@@ -17,6 +17,8 @@
 // (d, j) over columns in other components: Boruvka round 2 for free.
 #include <cstdint>
 #include <type_traits>
+#include <vector>
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -83,17 +85,61 @@ __device__ __forceinline__ void sym_load(SymStage& s, const double* __restrict__
     }
 }
 
-// Slot of the 1024-wide subtree of row i over super-block b.  One GPU:
-// [b][i] (G = 1, rows_pad = n).  Sharded (G ranks, rank r owning rows
-// [n*r/G, n*(r+1)/G)): [owner(i)][b][i - lo(owner)], so each owner's slots
-// are one contiguous chunk of an all-to-all.
-__host__ __device__ __forceinline__ int64_t ps_slot(int64_t b, int64_t i, int64_t n, int64_t nbs, int G,
-                                                    int64_t rows_pad) {
-    if (G == 1) return b * n + i;
-    int64_t r = i * G / n;
-    while (n * (r + 1) / G <= i) ++r;
-    while (n * r / G > i) --r;
-    return (r * nbs + b) * rows_pad + (i - n * r / G);
+// Slot of the 1024-wide subtree of row i over super-block b.
+//
+// One GPU: [b][i].
+//
+// Sharded (G ranks; rank r owns rows [n*r/G, n*(r+1)/G) and evaluates the
+// super-tiles (I, J), I <= J, J in its block range [jlo_r, jhi_r)): the
+// producer of slot (b, i) is the rank whose range holds max(b, B_i), B_i =
+// i / SB.  For a row in block B, rank s produces the contiguous block range
+//   b in [jlo_s, jhi_s)   when B <  jlo_s   (row role of its tiles)
+//   b in [0, jhi_s)       when B in [jlo_s, jhi_s) (column role below, row role from B)
+//   nothing               when B >= jhi_s.
+// The message s -> g holds exactly those slots for g's rows, row by row, so
+// every rank sends only what it produced (n * nbs slots over the whole job,
+// ~n * nbs / G per rank) -- an all-to-all with per-peer split sizes.  The
+// plan (host-built, uploaded per call) holds, for every (s, g), the offset
+// of the first row of g in block B within the message, and the send /
+// receive displacements:
+//   P[0, G) jlo, P[G, 2G) jhi, T[(s*G + g)*(nbs+1) + B], MC[s*G + g] (slots),
+//   SD[s*G + g] (send displacement of s's message to g),
+//   RD[g*G + s] (receive displacement of s's message at g).
+struct OmegaPlanView {
+    const int64_t* P;
+    int G;
+    int64_t n, nbs;
+    __host__ __device__ const int64_t* T() const { return P + 2 * G; }
+    __host__ __device__ const int64_t* MC() const { return P + 2 * G + (int64_t)G * G * (nbs + 1); }
+    __host__ __device__ const int64_t* SD() const { return MC() + G * G; }
+    __host__ __device__ const int64_t* RD() const { return SD() + G * G; }
+    // offset of slot (b, i) within the message s -> g (s produces it)
+    __host__ __device__ int64_t msg_off(int s, int g, int64_t i, int64_t b) const {
+        const int64_t B = i / SB, jlo = P[s], jhi = P[G + s];
+        const int64_t cnt = B < jlo ? jhi - jlo : (B < jhi ? jhi : 0);
+        const int64_t bst = B < jlo ? jlo : 0;
+        const int64_t lo_g = n * g / G;
+        const int64_t r0 = lo_g > B * SB ? lo_g : B * SB;
+        return T()[((int64_t)s * G + g) * (nbs + 1) + B] + (i - r0) * cnt + (b - bst);
+    }
+    __host__ __device__ int owner(int64_t i) const {
+        int64_t r = i * G / n;
+        while (n * (r + 1) / G <= i) ++r;
+        while (n * r / G > i) --r;
+        return (int)r;
+    }
+    __host__ __device__ int producer(int64_t b, int64_t B) const {
+        const int64_t m = b > B ? b : B;
+        for (int s = 0; s < G; ++s)
+            if (m >= P[s] && m < P[G + s]) return s;
+        return -1;
+    }
+};
+
+__device__ __forceinline__ int64_t ps_slot(int64_t b, int64_t i, int64_t n, const OmegaPlanView& pv, int rank) {
+    if (pv.P == nullptr) return b * n + i;
+    const int g = pv.owner(i);
+    return pv.SD()[rank * pv.G + g] + pv.msg_off(rank, g, i, b);
 }
 
 // Round-2 minima carry an exact-tie flag in the sign bit of the column
@@ -151,7 +197,7 @@ __device__ __forceinline__ void token_pass(int team) {
 __global__ void __launch_bounds__(STH, 1)
 omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n, int64_t nbs,
                  double sigma, double rs, const int32_t* __restrict__ comp, double* __restrict__ PS,
-                 double* __restrict__ PSm, int32_t* __restrict__ PSj, int64_t b0, int G, int64_t rows_pad) {
+                 double* __restrict__ PSm, int32_t* __restrict__ PSj, int64_t b0, OmegaPlanView pv, int rank) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SymSmem& sm = *reinterpret_cast<SymSmem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -400,7 +446,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                     } else {
                         const int64_t gi = R0 + ti * TBM + r;
                         if (gi < n) {
-                            const int64_t o = ps_slot(J, gi, n, nbs, G, rows_pad);
+                            const int64_t o = ps_slot(J, gi, n, pv, rank);
                             PS[o] = __dadd_rn(sm.rowv[r], half);
                             if (want_min) {
                                 double m = sm.rowm[r];
@@ -452,7 +498,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
         for (int c = ttid; c < HALF; c += TEAM) {
             const int64_t gj = C0 + c;
             if (gj < n) {
-                const int64_t o = ps_slot(I, gj, n, nbs, G, rows_pad);
+                const int64_t o = ps_slot(I, gj, n, pv, rank);
                 PS[o] = ts.cc[c][3];   // counter slot of the 8th row tile
                 if (want_min) { PSm[o] = ts.cmin[c]; PSj[o] = ts.cminj[c]; }
             }
@@ -460,23 +506,32 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
     }
 }
 
-// omega[i] = pow2 fold of PS[0..nbs)[i] (complete 1024-wide subtrees, zero
-// padded); round-2 minimum over the blocks (ties -> smaller column, flagged).  With G
-// senders (the sharded pass after its all-to-all) slot (g, b, r) sits at
-// (g * nbs + b) * stride + r and exactly one sender produced each (b, r);
-// the others hold 0 / (inf, INT32_MAX), so the sum over g is exact.
+// omega[i] = pow2 fold of the row's complete 1024-wide subtrees over the
+// super-blocks (zero padded); round-2 minimum over the blocks (ties ->
+// smaller column, flagged).  One GPU (pv.P == nullptr): slot (b, i) at
+// b * n + i.  Sharded: this owner's rows [row_lo, row_lo + rows), slot (b, i)
+// read from its producer's message in the received buffer.
 __global__ void omega_finish_kernel(const double* __restrict__ PS, const double* __restrict__ PSm,
-                                    const int32_t* __restrict__ PSj, int64_t rows, int64_t nbs, int G,
-                                    int64_t stride, double* __restrict__ omega, int32_t* __restrict__ nn_j,
-                                    double* __restrict__ nn_d, int8_t* __restrict__ nn_tie) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= rows) return;
+                                    const int32_t* __restrict__ PSj, int64_t row_lo, int64_t rows, int64_t n,
+                                    int64_t nbs, OmegaPlanView pv, int rank, double* __restrict__ omega,
+                                    int32_t* __restrict__ nn_j, double* __restrict__ nn_d,
+                                    int8_t* __restrict__ nn_tie) {
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= rows) return;
+    const int64_t i = row_lo + li;
+    const int64_t B = i / SB;
     double slots[40];
     double m = INFINITY;
     int32_t mj = INT32_MAX;
     for (int64_t b = 0; b < nbs; ++b) {
-        double v = PS[b * stride + i];
-        for (int g = 1; g < G; ++g) v = __dadd_rn(v, PS[((int64_t)g * nbs + b) * stride + i]);
+        int64_t o;
+        if (pv.P == nullptr) {
+            o = b * n + i;
+        } else {
+            const int s = pv.producer(b, B);
+            o = pv.RD()[rank * pv.G + s] + pv.msg_off(s, rank, i, b);
+        }
+        double v = PS[o];
         int lvl = 0;
         int64_t t = b;
         while (t & 1) {
@@ -485,12 +540,7 @@ __global__ void omega_finish_kernel(const double* __restrict__ PS, const double*
             ++lvl;
         }
         slots[lvl] = v;
-        if (PSm) {
-            for (int g = 0; g < G; ++g) {
-                const int64_t o = ((int64_t)g * nbs + b) * stride + i;
-                tie_merge(m, mj, PSm[o], PSj[o]);
-            }
-        }
+        if (PSm) tie_merge(m, mj, PSm[o], PSj[o]);
     }
     double acc = 0.0;
     bool have = false;
@@ -499,34 +549,83 @@ __global__ void omega_finish_kernel(const double* __restrict__ PS, const double*
             acc = have ? __dadd_rn(slots[lvl], acc) : slots[lvl];
             have = true;
         }
-    omega[i] = acc;
+    omega[li] = acc;
     if (PSm) {
-        nn_j[i] = jof(mj) == INT32_MAX ? -1 : jof(mj);
-        nn_d[i] = m;
-        nn_tie[i] = (int8_t)((mj & TIEBIT) != 0);
-    }
-}
-
-__global__ void omega_slots_fill_kernel(double* __restrict__ PS, double* __restrict__ PSm,
-                                        int32_t* __restrict__ PSj, int64_t total) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        PS[e] = 0.0;
-        if (PSm) { PSm[e] = INFINITY; PSj[e] = INT32_MAX; }
+        nn_j[li] = jof(mj) == INT32_MAX ? -1 : jof(mj);
+        nn_d[li] = m;
+        nn_tie[li] = (int8_t)((mj & TIEBIT) != 0);
     }
 }
 
 size_t omega_sym_smem() { return sizeof(SymSmem); }
 
-void omega_sym_shard_shape(int64_t n, int G, int64_t* nbs, int64_t* rows_pad) {
-    *nbs = (n + SB - 1) / SB;
-    *rows_pad = G == 1 ? n : (n + G - 1) / G;
+// Host-built plan of the sharded pass (layout: OmegaPlanView).
+void omega_plan_build(int64_t n, int G, std::vector<int64_t>& P) {
+    const int64_t nbs = (n + SB - 1) / SB;
+    const int64_t nT = (int64_t)G * G * (nbs + 1);
+    P.assign((size_t)(2 * G + nT + 3 * G * G), 0);
+    for (int s = 0; s < G; ++s) sym_block_range(n, s, G, &P[s], &P[G + s], SB);
+    int64_t* T = P.data() + 2 * G;
+    int64_t* MC = T + nT;
+    int64_t* SD = MC + G * G;
+    int64_t* RD = SD + G * G;
+    for (int s = 0; s < G; ++s) {
+        const int64_t jlo = P[s], jhi = P[G + s];
+        for (int g = 0; g < G; ++g) {
+            const int64_t lo_g = n * g / G, hi_g = n * (g + 1) / G;
+            int64_t acc = 0;
+            for (int64_t B = 0; B <= nbs; ++B) {
+                T[((int64_t)s * G + g) * (nbs + 1) + B] = acc;
+                if (B == nbs) break;
+                const int64_t a = std::max(lo_g, B * SB), e = std::min(hi_g, (B + 1) * SB);
+                const int64_t rows = e > a ? e - a : 0;
+                const int64_t cnt = B < jlo ? jhi - jlo : (B < jhi ? jhi : 0);
+                acc += rows * cnt;
+            }
+            MC[s * G + g] = acc;
+        }
+    }
+    for (int s = 0; s < G; ++s) {
+        int64_t a = 0;
+        for (int g = 0; g < G; ++g) { SD[s * G + g] = a; a += MC[s * G + g]; }
+    }
+    for (int g = 0; g < G; ++g) {
+        int64_t a = 0;
+        for (int s = 0; s < G; ++s) { RD[g * G + s] = a; a += MC[s * G + g]; }
+    }
+}
+
+void omega_shard_counts(int64_t n, int G, int rank, int64_t* send, int64_t* recv) {
+    std::vector<int64_t> P;
+    omega_plan_build(n, G, P);
+    const int64_t nbs = (n + SB - 1) / SB;
+    const int64_t* MC = P.data() + 2 * G + (int64_t)G * G * (nbs + 1);
+    for (int g = 0; g < G; ++g) {
+        send[g] = MC[rank * G + g];
+        recv[g] = MC[g * G + rank];
+    }
+}
+
+static cudaError_t upload_plan(int64_t n, int G, Scratch& sc, OmegaPlanView* pv, cudaStream_t st) {
+    std::vector<int64_t> P;
+    omega_plan_build(n, G, P);
+    int64_t* dP = nullptr;
+    cudaError_t e = sc.alloc(&dP, P.size());
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(dP, P.data(), P.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    pv->P = dP;
+    pv->G = G;
+    pv->n = n;
+    pv->nbs = (n + SB - 1) / SB;
+    // the host vector must outlive the copy
+    return cudaStreamSynchronize(st);
 }
 
 // Super-tiles (I, J), I <= J, J in [jlo, jhi) into the slot buffers (layout
-// of ps_slot).  Slots of other ranks' tiles are left to the caller's fill.
+// of ps_slot).
 static cudaError_t omega_sym_tiles(const double* X, int64_t n, int d, double sigma, const int32_t* comp,
-                                   int64_t jlo, int64_t jhi, int G, int64_t rows_pad, double* PS,
+                                   int64_t jlo, int64_t jhi, const OmegaPlanView& pv, int rank, double* PS,
                                    double* PSm, int32_t* PSj, cudaStream_t st) {
     const int64_t nbs = (n + SB - 1) / SB;
     const int64_t np = nbs * SB;
@@ -545,7 +644,7 @@ static cudaError_t omega_sym_tiles(const double* X, int64_t n, int d, double sig
     if (ctas > 0) {
         const int pid = prof_begin(PK_OMEGA, st);
         omega_sym_kernel<<<(unsigned)ctas, STH, smem, st>>>(XT, np, dpad, n, nbs, sigma, 1.0 / sigma, comp,
-                                                            PS, PSm, PSj, b0, G, rows_pad);
+                                                            PS, PSm, PSj, b0, pv, rank);
         prof_end(pid, st);
         note_launch(1);
     }
@@ -567,34 +666,39 @@ cudaError_t launch_omega_sym(const double* X, int64_t n, int d, double sigma, co
         e = sc.alloc(&PSj, (size_t)nbs * n);
         if (e != cudaSuccess) return e;
     }
-    e = omega_sym_tiles(X, n, d, sigma, comp, 0, nbs, 1, n, PS, PSm, PSj, st);
+    const OmegaPlanView one{nullptr, 1, n, nbs};
+    e = omega_sym_tiles(X, n, d, sigma, comp, 0, nbs, one, 0, PS, PSm, PSj, st);
     if (e != cudaSuccess) return e;
-    omega_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(PS, PSm, PSj, n, nbs, 1, n, omega, nn_j,
-                                                                     nn_d, nn_tie);
+    omega_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(PS, PSm, PSj, 0, n, n, nbs, one, 0, omega,
+                                                                     nn_j, nn_d, nn_tie);
     note_launch(1);
     return cudaGetLastError();
 }
 
 cudaError_t launch_omega_sym_range(const double* X, int64_t n, int d, double sigma, const int32_t* comp,
-                                   int64_t jlo, int64_t jhi, int G, double* PS, double* PSm, int32_t* PSj,
-                                   cudaStream_t st) {
-    int64_t nbs, rows_pad;
-    omega_sym_shard_shape(n, G, &nbs, &rows_pad);
-    const int64_t total = (int64_t)G * nbs * rows_pad;
-    omega_slots_fill_kernel<<<148 * 8, 256, 0, st>>>(PS, comp ? PSm : nullptr, PSj, total);
-    note_launch(1);
-    return omega_sym_tiles(X, n, d, sigma, comp, jlo, jhi, G, rows_pad, PS, comp ? PSm : nullptr,
+                                   int rank, int G, double* PS, double* PSm, int32_t* PSj, cudaStream_t st) {
+    Scratch sc(st);
+    OmegaPlanView pv;
+    cudaError_t e = upload_plan(n, G, sc, &pv, st);
+    if (e != cudaSuccess) return e;
+    int64_t jlo, jhi;
+    sym_block_range(n, rank, G, &jlo, &jhi, SB);
+    return omega_sym_tiles(X, n, d, sigma, comp, jlo, jhi, pv, rank, PS, comp ? PSm : nullptr,
                            comp ? PSj : nullptr, st);
 }
 
-cudaError_t launch_omega_rank_merge(int64_t n, int64_t lo, int64_t hi, int G, const double* PS,
-                                    const double* PSm, const int32_t* PSj, double* omega, int32_t* nn_j,
-                                    double* nn_d, int8_t* nn_tie, cudaStream_t st) {
-    int64_t nbs, rows_pad;
-    omega_sym_shard_shape(n, G, &nbs, &rows_pad);
+cudaError_t launch_omega_rank_merge(int64_t n, int rank, int G, const double* PS, const double* PSm,
+                                    const int32_t* PSj, double* omega, int32_t* nn_j, double* nn_d,
+                                    int8_t* nn_tie, cudaStream_t st) {
+    Scratch sc(st);
+    OmegaPlanView pv;
+    cudaError_t e = upload_plan(n, G, sc, &pv, st);
+    if (e != cudaSuccess) return e;
+    const int64_t lo = n * rank / G, hi = n * (rank + 1) / G;
     const int64_t rows = hi - lo;
-    omega_finish_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(PS, PSm, PSj, rows, nbs, G, rows_pad,
-                                                                        omega, nn_j, nn_d, nn_tie);
+    if (rows <= 0) return cudaSuccess;
+    omega_finish_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(PS, PSm, PSj, lo, rows, n, pv.nbs, pv,
+                                                                        rank, omega, nn_j, nn_d, nn_tie);
     note_launch(1);
     return cudaGetLastError();
 }

@@ -94,6 +94,17 @@ class Comm:
         self.dist.all_to_all_single(out, t)
         return out
 
+    def alltoall_var(self, t, send_counts, recv_counts):
+        """1-d `t` = this rank's messages to ranks 0..world-1 (send_counts
+        elements each, in rank order); returns the concatenation of the
+        messages every rank sent here (recv_counts elements each)."""
+        if self.world == 1:
+            return t
+        out = _torch().empty((max(1, sum(recv_counts)),), dtype=t.dtype, device=t.device)
+        self.dist.all_to_all_single(out[: sum(recv_counts)], t[: sum(send_counts)],
+                                    output_split_sizes=list(recv_counts), input_split_sizes=list(send_counts))
+        return out
+
     def allgather_stack(self, stack):
         """Fold stacks of every rank, in rank (= row) order."""
         if self.world == 1:
@@ -248,36 +259,39 @@ class CudaBackend:
                                       _ptr(nn_d), _ptr(nn_tie), self.stream))
         return out, (nn_j, nn_d, nn_tie)
 
-    def omega_shard_shape(self, n: int, G: int) -> tuple:
-        nbs, rows_pad = ctypes.c_int64(), ctypes.c_int64()
-        check(self.lib.isoc_omega_shard_shape(n, G, ctypes.byref(nbs), ctypes.byref(rows_pad)))
-        return int(nbs.value), int(rows_pad.value)
+    def omega_shard_counts(self, n: int, G: int, rank: int) -> tuple:
+        """Slots this rank sends to each owner / receives from each sender."""
+        send = (ctypes.c_int64 * G)()
+        recv = (ctypes.c_int64 * G)()
+        check(self.lib.isoc_omega_shard_counts(n, G, rank, send, recv))
+        return [int(v) for v in send], [int(v) for v in recv]
 
-    def omega_sym_range(self, X, n: int, d: int, jlo: int, jhi: int, sigma: float, G: int, h=None):
+    def omega_sym_range(self, X, n: int, d: int, rank: int, G: int, sigma: float, h=None):
         """This rank's flow subtrees (and, with the MST handle h, round-2
-        minima) per (row, super-block) slot, laid out (G, nbs, rows_pad)
-        by row owner: the send buffers of one all-to-all."""
+        minima): exactly the slots it produces, grouped by owner -- the send
+        buffers of one all-to-all with per-peer split sizes."""
         torch = self.torch
-        nbs, rows_pad = self.omega_shard_shape(n, G)
-        shape = (G, nbs, rows_pad)
-        ps = self.empty(shape, torch.float64)
-        psm = self.empty(shape, torch.float64) if h is not None else None
-        psj = self.empty(shape, torch.int32) if h is not None else None
-        check(self.lib.isoc_omega_sym_range(_ptr(X), n, d, jlo, jhi, float(sigma), h, G, _ptr(ps),
+        send, _ = self.omega_shard_counts(n, G, rank)
+        tot = max(1, sum(send))
+        ps = self.empty((tot,), torch.float64)
+        psm = self.empty((tot,), torch.float64) if h is not None else None
+        psj = self.empty((tot,), torch.int32) if h is not None else None
+        check(self.lib.isoc_omega_sym_range(_ptr(X), n, d, rank, G, float(sigma), h, _ptr(ps),
                                              None if psm is None else _ptr(psm),
                                              None if psj is None else _ptr(psj), self.stream))
         return ps, psm, psj
 
-    def omega_rank_merge(self, n: int, lo: int, hi: int, G: int, ps, psm=None, psj=None):
-        """Owner side: the G senders' slots for rows [lo, hi) -> (omega, nn)."""
+    def omega_rank_merge(self, n: int, rank: int, G: int, ps, psm=None, psj=None):
+        """Owner side: the senders' messages for this rank's rows -> (omega, nn)."""
         torch = self.torch
+        lo, hi = n * rank // G, n * (rank + 1) // G
         rows = hi - lo
         out = self.empty((rows,), torch.float64)
         nn = None
         if psm is not None:
             nn = (self.empty((rows,), torch.int32), self.empty((rows,), torch.float64),
                   self.empty((rows,), torch.int8))
-        check(self.lib.isoc_omega_rank_merge(n, lo, hi, G, _ptr(ps), None if psm is None else _ptr(psm),
+        check(self.lib.isoc_omega_rank_merge(n, rank, G, _ptr(ps), None if psm is None else _ptr(psm),
                                              None if psj is None else _ptr(psj), _ptr(out),
                                              *((None, None, None) if nn is None else tuple(_ptr(t) for t in nn)),
                                              self.stream))

@@ -158,16 +158,17 @@ def _sigma_pass(P: _Points, alpha: float, want_nn: bool = True):
 def _omega_pass(P: _Points, sigma: float, h=None):
     """This rank's omega rows (and, with the MST handle h, the exact round-2
     minima).  Multi-GPU with the symmetric split: every rank evaluates its
-    super-tile range once, one all-to-all per slot buffer delivers each
-    owner the (row, super-block) subtrees of its rows, and the owner folds
-    them -- bitwise the single-GPU result (each slot has one producer)."""
+    super-tile range once and sends each owner exactly the (row,
+    super-block) subtrees it produced for that owner's rows (one all-to-all
+    with per-peer split sizes per slot buffer); the owner folds them --
+    bitwise the single-GPU result (each slot has one producer)."""
     if _sharded_symmetric(P):
-        G = P.comm.world
-        jlo, jhi = P.b.omega_block_range(P.n, P.comm.rank, G)
-        ps, psm, psj = P.b.omega_sym_range(P.X, P.n, P.d, jlo, jhi, sigma, G, h)
-        recv = [None if t is None else P.comm.alltoall_chunks(t) for t in (ps, psm, psj)]
+        G, r = P.comm.world, P.comm.rank
+        send, recv_counts = P.b.omega_shard_counts(P.n, G, r)
+        ps, psm, psj = P.b.omega_sym_range(P.X, P.n, P.d, r, G, sigma, h)
+        recv = [None if t is None else P.comm.alltoall_var(t, send, recv_counts) for t in (ps, psm, psj)]
         del ps, psm, psj
-        return P.b.omega_rank_merge(P.n, P.lo, P.hi, G, *recv)
+        return P.b.omega_rank_merge(P.n, r, G, *recv)
     if h is None:
         return P.b.omega(P.X, P.n, P.d, P.lo, P.hi, sigma), None
     return P.b.omega_mst(P.X, P.n, P.d, P.lo, P.hi, sigma, h)

@@ -274,45 +274,83 @@ class EmuBackend:
     def omega_block_range(self, n, rank, world):
         return self.sym_block_range(n, rank, world, self.OMEGA_BLOCK)
 
-    def omega_shard_shape(self, n, G):
-        return -(-n // self.OMEGA_BLOCK), (n if G == 1 else -(-n // G))
+    def _omega_plan(self, n, G):
+        """omega_sym.cu omega_plan_build: per (sender s, owner g) message
+        offsets of the first row of g in each block, message sizes, send /
+        receive displacements."""
+        B = self.OMEGA_BLOCK
+        nbs = -(-n // B)
+        rng = [self.omega_block_range(n, s, G) for s in range(G)]
+        T = np.zeros((G, G, nbs + 1), np.int64)
+        for s, (jlo, jhi) in enumerate(rng):
+            for g in range(G):
+                lo_g, hi_g = n * g // G, n * (g + 1) // G
+                acc = 0
+                for blk in range(nbs + 1):
+                    T[s, g, blk] = acc
+                    if blk == nbs:
+                        break
+                    rows = max(0, min(hi_g, (blk + 1) * B) - max(lo_g, blk * B))
+                    cnt = jhi - jlo if blk < jlo else (jhi if blk < jhi else 0)
+                    acc += rows * cnt
+        MC = T[:, :, nbs]
+        return rng, T, MC, nbs
 
-    def omega_sym_range(self, X, n, d, jlo, jhi, sigma, G, h=None):
+    def omega_shard_counts(self, n, G, rank):
+        _, _, MC, _ = self._omega_plan(n, G)
+        return [int(v) for v in MC[rank, :]], [int(v) for v in MC[:, rank]]
+
+    def _msg_off(self, plan, n, G, s, g, i, b):
+        rng, T, _, _ = plan
+        B = self.OMEGA_BLOCK
+        blk = i // B
+        jlo, jhi = rng[s]
+        cnt = jhi - jlo if blk < jlo else (jhi if blk < jhi else 0)
+        bst = jlo if blk < jlo else 0
+        r0 = max(n * g // G, blk * B)
+        return int(T[s, g, blk]) + (i - r0) * cnt + (b - bst)
+
+    def omega_sym_range(self, X, n, d, rank, G, sigma, h=None):
         Xn = X.numpy()
         B = self.OMEGA_BLOCK
-        nbs, rows_pad = self.omega_shard_shape(n, G)
-        ps = np.zeros((G, nbs, rows_pad))
-        psm = np.full((G, nbs, rows_pad), np.inf)
-        psj = np.full((G, nbs, rows_pad), 2**31 - 1, np.int32)
+        plan = self._omega_plan(n, G)
+        rng, _, MC, nbs = plan
+        jlo, jhi = rng[rank]
+        sd = np.concatenate([[0], np.cumsum(MC[rank, :])])
+        tot = max(1, int(sd[-1]))
+        ps = np.zeros(tot)
+        psm = np.full(tot, np.inf)
+        psj = np.full(tot, 2**31 - 1, np.int32)
         D = orc.distance_rows(Xn, 0, n)
         F = orc.exp(np.negative(D) / sigma)
         np.fill_diagonal(F, 0.0)
         Fp = np.zeros((n, nbs * B))
         Fp[:, :n] = F
 
-        def slot(b, i):
+        def owner(i):
             r = i * G // n
             while n * (r + 1) // G <= i:
                 r += 1
             while n * r // G > i:
                 r -= 1
-            return r, b, i - n * r // G
+            return r
 
         def put(i, b):
             seg = Fp[i, b * B:(b + 1) * B]
             while seg.size > 1:
                 seg = seg[0::2] + seg[1::2]
-            s = slot(b, i)
-            ps[s] = seg[0]
+            g = owner(i)
+            o = int(sd[g]) + self._msg_off(plan, n, G, rank, g, i, b)
+            ps[o] = seg[0]
             if h is not None:
                 row = D[i, b * B:min((b + 1) * B, n)].copy()
                 row[h.comp[b * B:b * B + row.size] == h.comp[i]] = np.inf
                 if row.size and np.isfinite(row.min()):
                     j = int(np.argmin(row))
-                    psm[s] = row[j]
+                    psm[o] = row[j]
                     # exact tie flag in the index's sign bit (omega_sym.cu TIEBIT)
                     tie = int(np.count_nonzero(row == row[j]) > 1)
-                    psj[s] = np.int32(np.uint32((b * B + j) | (tie << 31)).view(np.int32))
+                    psj[o] = np.int32(np.uint32((b * B + j) | (tie << 31)).view(np.int32))
 
         for J in range(jlo, jhi):
             for I in range(J + 1):
@@ -324,33 +362,40 @@ class EmuBackend:
         t = torch.from_numpy
         return t(ps), (t(psm) if h is not None else None), (t(psj) if h is not None else None)
 
-    def omega_rank_merge(self, n, lo, hi, G, ps, psm=None, psj=None):
+    def omega_rank_merge(self, n, rank, G, ps, psm=None, psj=None):
+        plan = self._omega_plan(n, G)
+        rng, _, MC, nbs = plan
+        rd = np.concatenate([[0], np.cumsum(MC[:, rank])])
         P = ps.numpy()
-        nbs = P.shape[1]
+        lo, hi = n * rank // G, n * (rank + 1) // G
         om = np.empty(hi - lo)
         nn_j = np.full(hi - lo, -1, np.int32)
         nn_d = np.full(hi - lo, np.inf)
         nn_t = np.zeros(hi - lo, np.int8)
+        B = self.OMEGA_BLOCK
         for q in range(hi - lo):
-            v = P[0, :, q].copy()
-            for g in range(1, G):
-                v = v + P[g, :, q]
+            i = lo + q
+            blk = i // B
+            offs = []
+            for b in range(nbs):
+                m = max(b, blk)
+                s = next(s for s, (a, e) in enumerate(rng) if a <= m < e)
+                offs.append(int(rd[s]) + self._msg_off(plan, n, G, s, rank, i, b))
             w = np.zeros(1 << max(0, (nbs - 1).bit_length()))
-            w[:nbs] = v
+            w[:nbs] = P[offs]
             while w.size > 1:
                 w = w[0::2] + w[1::2]
             om[q] = w[0]
             if psm is not None:
                 m, mj, tie = np.inf, 2**31 - 1, 0
-                for g in range(G):
-                    for b in range(nbs):
-                        x = float(psm[g, b, q])
-                        raw = int(np.int32(psj[g, b, q]).view(np.uint32))
-                        xj, xt = raw & 0x7FFFFFFF, raw >> 31
-                        if x < m:
-                            m, mj, tie = x, xj, xt
-                        elif x == m and np.isfinite(x):
-                            mj, tie = min(mj, xj), 1
+                for o in offs:
+                    x = float(psm[o])
+                    raw = int(np.int32(psj[o]).view(np.uint32))
+                    xj, xt = raw & 0x7FFFFFFF, raw >> 31
+                    if x < m:
+                        m, mj, tie = x, xj, xt
+                    elif x == m and np.isfinite(x):
+                        mj, tie = min(mj, xj), 1
                 if mj != 2**31 - 1:
                     nn_j[q], nn_d[q], nn_t[q] = mj, m, tie
         nn = None

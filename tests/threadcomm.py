@@ -65,5 +65,15 @@ class ThreadComm:
         self.g.exchange(self.rank, None)
         return out
 
+    def alltoall_var(self, t, send_counts, recv_counts):
+        parts = self.g.exchange(self.rank, (t, list(send_counts)))
+        segs = []
+        for buf, cnts in parts:
+            off = sum(cnts[: self.rank])
+            segs.append(buf[off: off + cnts[self.rank]])
+        out = torch.cat(segs).contiguous()
+        self.g.exchange(self.rank, None)
+        return out
+
     def allgather_stack(self, stack):
         return torch.stack(self.g.exchange(self.rank, stack.clone()))
