@@ -100,6 +100,7 @@ SIGNATURES = {
     "isoc_tree_set_weights": (ctypes.c_int, [P, P, P, P]),
     "isoc_decide": (ctypes.c_int, [P, D, I64, I32, PI64]),
     "isoc_witness": (ctypes.c_int, [P, I32, I64, P, P, P, P, PD]),
+    "isoc_decide_batch_capacity": (ctypes.c_int, [P, P]),
     "isoc_decide_batch": (ctypes.c_int, [P, P, I32, I64, P]),
     "isoc_tree_shape": (ctypes.c_int, [P, PI64, PI64]),
     "isoc_tree_destroy": (None, [P]),

@@ -635,7 +635,7 @@ struct isoc_tree {
     int32_t *excl, *scratch;
     int64_t* j_out;
     // batched speculative sweeps (isoc_decide_batch), allocated on first use
-    int32_t bcap;
+    int32_t bcap, bcap_small;
     double *bom, *bp, *bthr;
     int8_t* bcode;
     int32_t *bexcl, *bscratch;
@@ -873,10 +873,41 @@ int isoc_tree_shape(isoc_tree* t, int64_t* levels, int64_t* max_width) {
     return ISOC_OK;
 }
 
+int isoc_decide_batch_capacity(isoc_tree* t, int32_t* cap) {
+    if (!t || !cap) return fail(ISOC_EINVAL, "null argument");
+    size_t smem = 0;
+    *cap = decide_small_fits(t->n, t->levels, &smem) ? DECIDE_SMALL_MAX_BATCH : 16;
+    return ISOC_OK;
+}
+
 int isoc_decide_batch(isoc_tree* t, const double* thresholds, int32_t count, int64_t k, int64_t* j_host) {
     if (!t->omega_v) return fail(ISOC_EINVAL, "weights not attached");
     if (k < 1) return fail(ISOC_EINVAL, "k must be >= 1, got %lld", (long long)k);
-    if (count < 1 || count > 16) return fail(ISOC_EINVAL, "batch of %d thresholds (1..16)", count);
+    int32_t cap = 16;
+    isoc_decide_batch_capacity(t, &cap);
+    if (count < 1 || count > cap) return fail(ISOC_EINVAL, "batch of %d thresholds (1..%d)", count, cap);
+    size_t smem_small = 0;
+    if (decide_small_fits(t->n, t->levels, &smem_small)) {
+        // one warp per threshold in shared memory: only thresholds and counts on the device
+        cudaStream_t st = t->st;
+        if (t->bcap_small < count) {
+            if (t->bthr) cudaFreeAsync(t->bthr, st);
+            if (t->bj) cudaFreeAsync(t->bj, st);
+            t->bthr = nullptr;
+            t->bj = nullptr;
+            t->bcap = 0;
+            CK(dalloc(&t->bthr, DECIDE_SMALL_MAX_BATCH, st));
+            CK(dalloc(&t->bj, DECIDE_SMALL_MAX_BATCH, st));
+            t->bcap_small = DECIDE_SMALL_MAX_BATCH;
+        }
+        CK(cudaMemcpyAsync(t->bthr, thresholds, (size_t)count * 8, cudaMemcpyHostToDevice, st));
+        CK(launch_decide_batch(t->n, t->levels, t->level_off, t->max_width, t->f_pos, t->om_pos, t->p_pos,
+                               t->child_lo, t->child_cnt, t->bthr, count, k, nullptr, nullptr, nullptr,
+                               nullptr, nullptr, t->bj, st));
+        CK(cudaMemcpyAsync(j_host, t->bj, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return ISOC_OK;
+    }
     for (int i = 0; i < count; ++i)
         if (!std::isfinite(thresholds[i])) return fail(ISOC_EINVAL, "threshold must be finite, got %g", thresholds[i]);
     cudaStream_t st = t->st;

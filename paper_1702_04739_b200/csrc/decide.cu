@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1) decide_small_kernel(DecideSmall
     if (lane == 0) A.j_out[blockIdx.x] = j;
 }
 
-static bool decide_small_fits(int64_t n, int64_t levels, size_t* smem) {
+bool decide_small_fits(int64_t n, int64_t levels, size_t* smem) {
     *smem = decide_small_smem(n, levels);
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);

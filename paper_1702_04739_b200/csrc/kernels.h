@@ -97,6 +97,9 @@ cudaError_t launch_hook_contract(int32_t* comp, int64_t n, const unsigned long l
 size_t tc_image_bytes(int64_t n, int d);
 cudaError_t launch_tc_image(const float* YT, int64_t npad, int d, float scale, int64_t n, uint8_t* img,
                             cudaStream_t st);
+// small trees: the whole sweep in one CTA's shared memory (decide_small_kernel)
+bool decide_small_fits(int64_t n, int64_t levels, size_t* smem);
+constexpr int DECIDE_SMALL_MAX_BATCH = 63;   // thresholds per batched small sweep (one warp each)
 // candidate lists per row: FILTER_LIST_K best (a, j) + the bound of the rest
 #define FILTER_LIST_K 8
 // rows_map == nullptr: every row of [lo, hi); else the nmap rows listed

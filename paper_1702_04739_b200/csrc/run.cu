@@ -238,10 +238,13 @@ int run_impl(const double* points, int64_t n, int32_t d, int64_t k, double sigma
     {
         int64_t levels = 1, width = 0;
         RCK(isoc_tree_shape(tree, &levels, &width));
-        m = (n <= 64 * 1024 * (levels > 1 ? levels : 1) && width <= 262144) ? 4 : 1;
+        int32_t cap = 16;
+        RCK(isoc_decide_batch_capacity(tree, &cap));
+        const int mmax = cap >= 63 ? 6 : 4;
+        m = cap >= 63 ? 6 : ((n <= 64 * 1024 * (levels > 1 ? levels : 1) && width <= 262144) ? 4 : 1);
         if (const char* e = getenv("ISOC_SPEC_M")) {
             m = atoi(e);
-            m = m < 1 ? 1 : (m > 4 ? 4 : m);
+            m = m < 1 ? 1 : (m > mmax ? mmax : m);
         }
     }
     if (m <= 1) {
@@ -267,13 +270,13 @@ int run_impl(const double* points, int64_t n, int32_t d, int64_t k, double sigma
         bool have_w = false, stop = false;
         double wthr = 0.0;
         while (!stop && iters < t_budget) {
-            double thr[16];
-            int kid[16][2];
+            double thr[64];
+            int kid[64][2];
             int cnt = 0;
             const int64_t depth = (m < t_budget - iters) ? m : (t_budget - iters);
             // iterative build in the same preorder as the Python recursion
             struct Frame { double a, b; int depth, parent, side; };
-            Frame stk[64];
+            Frame stk[128];
             int sp = 0;
             stk[sp++] = {lo, hi, (int)depth, -1, 0};
             int root = -1;
@@ -293,7 +296,7 @@ int run_impl(const double* points, int64_t n, int32_t d, int64_t k, double sigma
                 else kid[f.parent][f.side] = idx;
             }
             if (root < 0) break;
-            int64_t js[16];
+            int64_t js[64];
             RCK(isoc_decide_batch(tree, thr, cnt, k, js));
             int node = root;
             while (node >= 0) {

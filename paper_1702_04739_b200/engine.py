@@ -435,7 +435,7 @@ class DeviceTree:
         return int(j.value)
 
     def decide_batch(self, thresholds, k: int) -> list:
-        """Cut counts j at up to 16 thresholds in one level-synchronous pass."""
+        """Cut counts j at up to batch_capacity() thresholds in one level-synchronous pass."""
         thr = np.ascontiguousarray(thresholds, dtype=np.float64)
         j = np.empty(thr.shape[0], np.int64)
         check(self.b.lib.isoc_decide_batch(self.h, thr.ctypes.data, int(thr.shape[0]), int(k), j.ctypes.data))
@@ -447,6 +447,13 @@ class DeviceTree:
         miso = ctypes.c_double()
         check(self.b.lib.isoc_tree_cost(self.h, _ptr(lab), int(k), ctypes.byref(miso)))
         return float(miso.value)
+
+    def batch_capacity(self) -> int:
+        """Thresholds per isoc_decide_batch: 63 on trees that fit one CTA's
+        shared memory (one warp each), else 16."""
+        cap = ctypes.c_int32()
+        check(self.b.lib.isoc_decide_batch_capacity(self.h, ctypes.byref(cap)))
+        return int(cap.value)
 
     def shape(self) -> tuple:
         lv, mw = ctypes.c_int64(), ctypes.c_int64()

@@ -381,17 +381,22 @@ par_decide = decide
 
 
 def _speculation_depth(dt: DeviceTree) -> int:
-    """Bisection steps per batched sweep: 4 (15 thresholds, one CTA group
-    each) on latency-bound trees whose levels are narrow (MST trees of
+    """Bisection steps per batched sweep: 6 (63 thresholds, one warp each)
+    on trees that fit one CTA's shared memory (C1), 4 (15 thresholds, one
+    CTA group each) on latency-bound trees whose levels are narrow (MST trees of
     C1-C4), 1 (plain sequential sweeps, which stop at their own k-th cut) on
     wide trees (C5): there a 3-threshold sweep -- split CTAs or shared
     (decide_multi_kernel) -- costs 2.3x a single one.  ISOC_SPEC_M
     overrides."""
+    cap = dt.batch_capacity() if hasattr(dt, "batch_capacity") else 16
+    mmax = 6 if cap >= 63 else 4
     env = os.environ.get("ISOC_SPEC_M")
     if env is not None:
-        return max(1, min(4, int(env)))
+        return max(1, min(mmax, int(env)))
     if not hasattr(dt, "shape"):
         return 1
+    if cap >= 63:
+        return 6   # small tree: one warp per threshold, 63 thresholds cost one sweep
     levels, width = dt.shape()
     return 4 if dt.n <= 64 * 1024 * max(1, levels) and width <= 262144 else 1
 
