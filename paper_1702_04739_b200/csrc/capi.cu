@@ -571,17 +571,20 @@ int isoc_omega_mst(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi
     const int32_t* comp = h ? h->comp : nullptr;
     if (h && (h->lo != lo || h->hi != hi)) return fail(ISOC_EINVAL, "MST handle rows differ");
     // the symmetric pass keeps one 1024-wide subtree (+ round-2 minimum) per
-    // (block, row): 20 B x n^2 / 1024 -- use it while that fits comfortably
+    // (block, row): 20 B x n^2 / 1024 -- use it while that fits comfortably,
+    // and once its I <= J super-tiles fill the SMs (n >~ 17k); below that the
+    // row pass finishes sooner (bitwise identical)
     const int64_t nbs = (n + 1023) / 1024;
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const double ps_bytes = (double)nbs * (double)n * (comp ? 20.0 : 8.0);
-    const bool sym_fits = ps_bytes < 0.6 * (double)free_b;
-    // the symmetric pass once its I <= J super-tiles fill the SMs (n >~ 17k);
-    // below that the row pass finishes sooner (bitwise identical)
     const int mode = passes_mode();
     const bool sym_wide = mode == 1 || (mode == 0 && nbs * (nbs + 1) / 2 >= device_sm_count());
-    if (lo == 0 && hi == n && sym_fits && sym_wide) {
+    bool sym = lo == 0 && hi == n && sym_wide;
+    if (sym) {   // (cudaMemGetInfo costs ~1 ms: only when the symmetric pass is a candidate)
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        const double ps_bytes = (double)nbs * (double)n * (comp ? 20.0 : 8.0);
+        sym = ps_bytes < 0.6 * (double)free_b;
+    }
+    if (sym) {
         CK(launch_omega_sym(X, n, d, sigma, comp, omega, nn_j, nn_d, nn_tie, (cudaStream_t)stream));
     } else {
         CK(launch_omega_pass(X, n, d, lo, hi, sigma, comp, omega, nn_j, nn_d, nn_tie,

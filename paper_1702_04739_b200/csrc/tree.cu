@@ -412,6 +412,99 @@ cudaError_t launch_children_from_parent(const int64_t* parent, const int64_t* ch
     return cudaGetLastError();
 }
 
+// Small trees (n <= BFS_SMALL_N, e.g. C1's 228-level MST): one warp walks the
+// levels with the adjacency, BFS order and parents in shared memory, so a
+// level costs shuffles and shared-memory latencies instead of two grid
+// barriers over global memory.  Same outputs and order as bfs_kernel
+// (children in adjacency order, i.e. Prim's (d, id) rank for the MST).
+constexpr int64_t BFS_SMALL_N = 8192;
+
+__global__ void __launch_bounds__(32, 1) bfs_small_kernel(BfsArgs A) {
+    extern __shared__ __align__(16) unsigned char bs_raw[];
+    const int lane = threadIdx.x;
+    const int64_t n = A.n;
+    int32_t* off = reinterpret_cast<int32_t*>(bs_raw);
+    const int64_t m = A.off[n];
+    int32_t* adj = off + n + 1;
+    int32_t* bfs = adj + m;
+    int32_t* par = bfs + n;
+    for (int64_t q = lane; q <= n; q += 32) off[q] = A.off[q];
+    for (int64_t q = lane; q < m; q += 32) adj[q] = A.adj[q];
+    __syncwarp();
+    if (lane == 0) {
+        bfs[0] = (int32_t)A.root;
+        par[A.root] = -1;
+        A.bfs[0] = (int32_t)A.root;
+        A.pos_of[A.root] = 0;
+        A.parent_v[A.root] = -1;
+        A.depth_v[A.root] = 0;
+        A.pos_parent[0] = -1;
+        if (A.undirected) { A.child_id_v[A.root] = 0; A.parent_d[A.root] = 0.0; }
+        A.level_off[0] = 0;
+        A.level_off[1] = 1;
+    }
+    __syncwarp();
+    int64_t lo = 0, hi = 1;
+    int level = 0;
+    while (true) {
+        int64_t carry = 0;
+        for (int64_t base = lo; base < hi; base += 32) {
+            const int64_t p = base + lane;
+            int32_t v = 0, c = 0;
+            if (p < hi) {
+                v = bfs[p];
+                c = off[v + 1] - off[v];
+                if (A.undirected && v != A.root) c -= 1;
+            }
+            int32_t x = c;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (p < hi) {
+                const int64_t first = hi + carry + x - c;
+                const int32_t pv = par[v];
+                int32_t rank = 0;
+                for (int32_t e = off[v]; e < off[v + 1]; ++e) {
+                    const int32_t w = adj[e];
+                    if (A.undirected && w == pv) continue;
+                    const int64_t q = first + rank;
+                    if (q < n) {
+                        bfs[q] = w;
+                        par[w] = v;
+                        A.bfs[q] = w;
+                        A.pos_of[w] = (int32_t)q;
+                        A.parent_v[w] = v;
+                        A.depth_v[w] = level + 1;
+                        A.pos_parent[q] = (int32_t)p;
+                        if (A.undirected) {
+                            A.child_id_v[w] = rank;
+                            A.parent_d[w] = A.adjd[e];
+                        }
+                    }
+                    ++rank;
+                }
+                A.child_lo[p] = (int32_t)first;
+                A.child_cnt[p] = rank;
+            }
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        __syncwarp();
+        if (lane == 0) A.level_off[level + 2] = hi + carry;
+        if (carry == 0) {
+            if (lane == 0) *A.out_levels = level + 1;
+            break;
+        }
+        lo = hi;
+        hi = hi + carry;
+        ++level;
+        if (hi > n) {  // not a tree (cycle); stop
+            if (lane == 0) *A.out_levels = -1;
+            break;
+        }
+    }
+}
+
 int bfs_grid_size(int64_t n) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
@@ -428,7 +521,8 @@ cudaError_t launch_bfs(int64_t n, int64_t root, int undirected, const int32_t* o
                        int32_t* parent_v, int32_t* depth_v, int32_t* child_id_v, double* parent_d,
                        int32_t* pos_parent, int32_t* child_lo, int32_t* child_cnt,
                        int64_t* level_off, int32_t* scratch, int64_t* out_levels, cudaStream_t st) {
-    const int G = bfs_grid_size(n);
+    const bool small = n <= BFS_SMALL_N;
+    const int G = small ? 1 : bfs_grid_size(n);
     BfsArgs A;
     A.n = n; A.root = root; A.undirected = undirected; A.off = off; A.adj = adj; A.adjd = adjd;
     A.bfs = bfs; A.pos_of = pos_of; A.parent_v = parent_v; A.depth_v = depth_v;
@@ -439,6 +533,19 @@ cudaError_t launch_bfs(int64_t n, int64_t root, int undirected, const int32_t* o
     A.bar = reinterpret_cast<unsigned int*>(scratch + n + G + 2);
     A.out_levels = out_levels;
     cudaMemsetAsync(A.bar, 0, 2 * sizeof(unsigned int), st);
+    if (small) {
+        // off (n+1) + adj (<= 2n) + bfs (n) + parents (n), int32: the adjacency
+        // length is read on the device, so size for the undirected maximum
+        const size_t smem = (size_t)(n + 1 + 2 * n + 2 * n) * sizeof(int32_t);
+        cudaError_t e = cudaFuncSetAttribute(bfs_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        const int pid = prof_begin(PK_BFS, st);
+        bfs_small_kernel<<<1, 32, smem, st>>>(A);
+        prof_end(pid, st);
+        note_launch();
+        return cudaGetLastError();
+    }
     void* args[] = {&A};
     const int pid = prof_begin(PK_BFS, st);
     cudaError_t e = cudaLaunchCooperativeKernel((void*)bfs_kernel, dim3(G), dim3(512), args, 0, st);

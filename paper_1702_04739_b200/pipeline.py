@@ -401,6 +401,38 @@ def _speculation_depth(dt: DeviceTree) -> int:
     return 4 if dt.n <= 64 * 1024 * max(1, levels) and width <= 262144 else 1
 
 
+def _threshold_tree(a0: float, b0: float, depth: int):
+    """The midpoints the next `depth` bisection steps can visit from the
+    bracket (a0, b0): node = (a + b) / 2 of its interval, children the
+    halves (a, mid) and (mid, b); a node whose interval already passes the
+    reference's stop test b - a <= 1e-15 * max(1, b) (isoperim.py:263-266)
+    does not exist, nor do its descendants.  Built in level order.  Returns
+    (thresholds, kids[node] = [left, right] or -1, root or -1)."""
+    thr: list = []
+    kids: list = []
+    root = -1
+    cur = [(a0, b0, -1, 0)]
+    for _ in range(depth):
+        nxt = []
+        for a, b, par, side in cur:
+            if b - a <= BRACKET_EPS * max(1.0, b):
+                continue
+            mid = (a + b) / 2.0
+            idx = len(thr)
+            thr.append(mid)
+            kids.append([-1, -1])
+            if par < 0:
+                root = idx
+            else:
+                kids[par][side] = idx
+            nxt.append((a, mid, idx, 0))
+            nxt.append((mid, b, idx, 1))
+        if not nxt:
+            break
+        cur = nxt
+    return thr, kids, root
+
+
 def run_bisection(dt: DeviceTree, ext: Extrema, k: int, n: int) -> MisoResult:
     """isoperim.py:222-308 with device decision sweeps.
 
@@ -456,20 +488,7 @@ def run_bisection(dt: DeviceTree, ext: Extrema, k: int, n: int) -> MisoResult:
         wthr = None
         stop = False
         while not stop and rounds < t:
-            thr: list = []
-            kids: list = []
-
-            def build(a: float, b: float, depth: int) -> int:
-                if depth == 0 or b - a <= BRACKET_EPS * max(1.0, b):
-                    return -1
-                mid = (a + b) / 2.0
-                idx = len(thr)
-                thr.append(mid)
-                kids.append(None)
-                kids[idx] = (build(a, mid, depth - 1), build(mid, b, depth - 1))
-                return idx
-
-            root = build(alpha, beta, min(m, t - rounds))
+            thr, kids, root = _threshold_tree(alpha, beta, min(m, t - rounds))
             if root < 0:
                 break
             js = dt.decide_batch(thr, k)

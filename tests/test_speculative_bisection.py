@@ -103,3 +103,44 @@ def test_speculation_depth_heuristic(monkeypatch):
     monkeypatch.delenv("ISOC_SPEC_M", raising=False)
     assert pipeline._speculation_depth(FakeTree(1_000_000, 5, 0.0, levels=200, width=20_000)) == 4
     assert pipeline._speculation_depth(FakeTree(50_000_000, 5, 0.0, levels=35, width=4_000_000)) == 1
+
+
+def test_threshold_tree_walks_equal_recursive_build():
+    """pipeline._threshold_tree (level order) offers the walk exactly the
+    midpoints of the recursive preorder build, for every outcome pattern."""
+    import random
+    from paper_1702_04739_b200.pipeline import BRACKET_EPS, _threshold_tree
+
+    def build_rec(a0, b0, depth):
+        thr, kids = [], []
+
+        def build(a, b, d):
+            if d == 0 or b - a <= BRACKET_EPS * max(1.0, b):
+                return -1
+            mid = (a + b) / 2.0
+            idx = len(thr)
+            thr.append(mid)
+            kids.append(None)
+            kids[idx] = (build(a, mid, d - 1), build(mid, b, d - 1))
+            return idx
+        return thr, kids, build(a0, b0, depth)
+
+    def walk(thr, kids, root, pat):
+        node, out, bit = root, [], 0
+        while node >= 0:
+            ok = (pat >> bit) & 1
+            bit += 1
+            out.append(thr[node])
+            node = kids[node][0] if ok else kids[node][1]
+        return out
+
+    rng = random.Random(3)
+    for _ in range(500):
+        a = rng.random() * rng.choice([1e-8, 1.0, 1e3])
+        b = a + rng.random() * rng.choice([1e-20, 1e-14, 1e-6, 1.0, 10.0])
+        d = rng.randint(1, 6)
+        t1, k1, r1 = build_rec(a, b, d)
+        t2, k2, r2 = _threshold_tree(a, b, d)
+        assert sorted(t1) == sorted(t2)
+        for pat in range(1 << d):
+            assert walk(t1, k1, r1, pat) == walk(t2, k2, r2, pat)
