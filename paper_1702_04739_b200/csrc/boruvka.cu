@@ -826,6 +826,47 @@ cudaError_t launch_list_refresh(const float* a1, const float* lbo, const float* 
     return cudaGetLastError();
 }
 
+// Tiny problems (n^2 d small, e.g. C1): every row is rescanned exactly --
+// the tiled exact rescan over all rows costs less than a filter launch, its
+// list bookkeeping and the host round trip of a refresh.
+__global__ void all_rows_rescan_kernel(int64_t lo, int64_t hi, int8_t* __restrict__ cand_state,
+                                       int32_t* __restrict__ rescan_list, int32_t* __restrict__ rescan_count) {
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li == 0) *rescan_count = (int32_t)(hi - lo);
+    if (li >= hi - lo) return;
+    cand_state[li] = 2;
+    rescan_list[li] = (int32_t)(lo + li);
+}
+
+cudaError_t launch_boruvka_exact_all(const double* X, int64_t n, int d, const int32_t* comp, int64_t lo,
+                                     int64_t hi, double* cand_d, int32_t* cand_j, int8_t* cand_state,
+                                     int8_t* cand_tie, int32_t* rescan_list, int32_t* rescan_count,
+                                     cudaStream_t st) {
+    const int64_t rows = hi - lo;
+    if (rows <= 0) return cudaSuccess;
+    cudaMemsetAsync(cand_tie, 0, (size_t)rows, st);
+    all_rows_rescan_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(lo, hi, cand_state, rescan_list, rescan_count);
+    const int64_t nchunks = (n + RCW - 1) / RCW;
+    double *pm1 = nullptr, *pm2 = nullptr;
+    int32_t* pj = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&pm1, (size_t)rows * nchunks * 8, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMallocAsync((void**)&pm2, (size_t)rows * nchunks * 8, st);
+    if (e != cudaSuccess) { cudaFreeAsync(pm1, st); return e; }
+    e = cudaMallocAsync((void**)&pj, (size_t)rows * nchunks * 4, st);
+    if (e != cudaSuccess) { cudaFreeAsync(pm1, st); cudaFreeAsync(pm2, st); return e; }
+    const int pid = prof_begin(PK_RESCAN, st);
+    rescan_tile_kernel<<<148 * 3, 256, 0, st>>>(X, n, d, comp, rescan_list, rescan_count, nchunks, pm1, pm2, pj);
+    rescan_reduce_kernel<<<148, 256, 0, st>>>(rescan_list, rescan_count, lo, nchunks, pm1, pm2, pj, cand_d,
+                                              cand_j, cand_tie);
+    prof_end(pid, st);
+    note_launch(3);
+    cudaFreeAsync(pm1, st);
+    cudaFreeAsync(pm2, st);
+    cudaFreeAsync(pj, st);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_nn_candidates(const int32_t* nn_j, const double* nn_d, const int8_t* nn_tie,
                                  int64_t rows, double* cand_d, int32_t* cand_j, int8_t* cand_state,
                                  int8_t* cand_tie, cudaStream_t st) {

@@ -320,7 +320,7 @@ struct isoc_mst {
     int32_t d, dp;
     cudaStream_t st;
     float cd, cabs;
-    int use_tc;
+    int use_tc, filter_forced;
     float kscale;
     uint8_t* img;
     float *Y, *ny, *rad;
@@ -410,6 +410,7 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
     // tensor-core filter (tcgen05, 3-term FP16 split) for d <= 64 unless ISOC_FILTER=ffma
     const char* fenv = getenv("ISOC_FILTER");
     h->use_tc = (d <= 512) && !(fenv && strcmp(fenv, "ffma") == 0);
+    h->filter_forced = fenv != nullptr;
     if (h->use_tc) {
         uint32_t* am = nullptr;
         MCK(dalloc(&am, 1, h->st));
@@ -455,6 +456,11 @@ int isoc_mst_round_local(isoc_mst* h, int use_nn, const int32_t* nn_j, const dou
     if (use_nn) {
         CK(launch_nn_candidates(nn_j, nn_d, nn_tie, h->rows, h->cand_d, h->cand_j, h->cand_state,
                                 h->cand_tie, st));
+    } else if ((double)h->n * (double)h->n * (double)h->d <= 2.0e8 && !h->filter_forced) {
+        // tiny problem: exact rescans of every row beat the filter's launches
+        // (ISOC_FILTER=tc|ffma forces a filter: tests)
+        CK(launch_boruvka_exact_all(h->X, h->n, h->d, h->comp, h->lo, h->hi, h->cand_d, h->cand_j,
+                                    h->cand_state, h->cand_tie, h->rescan_list, h->counters + 0, st));
     } else {
         if (h->use_tc) {
             // candidate lists: the first filter round scans every block; later

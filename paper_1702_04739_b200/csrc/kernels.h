@@ -74,6 +74,10 @@ cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float
                                   int64_t lo, int64_t hi, uint32_t* compB, double* cand_d,
                                   int32_t* cand_j, int8_t* cand_state, int8_t* cand_tie,
                                   int32_t* rescan_list, int32_t* rescan_count, cudaStream_t st);
+cudaError_t launch_boruvka_exact_all(const double* X, int64_t n, int d, const int32_t* comp, int64_t lo,
+                                     int64_t hi, double* cand_d, int32_t* cand_j, int8_t* cand_state,
+                                     int8_t* cand_tie, int32_t* rescan_list, int32_t* rescan_count,
+                                     cudaStream_t st);
 cudaError_t launch_nn_candidates(const int32_t* nn_j, const double* nn_d, const int8_t* nn_tie,
                                  int64_t rows, double* cand_d, int32_t* cand_j, int8_t* cand_state,
                                  int8_t* cand_tie, cudaStream_t st);
