@@ -105,7 +105,7 @@ cudaError_t launch_tc_image(const float* YT, int64_t npad, int d, float scale, i
 bool decide_small_fits(int64_t n, int64_t levels, size_t* smem);
 constexpr int DECIDE_SMALL_MAX_BATCH = 63;   // thresholds per batched small sweep (one warp each)
 // candidate lists per row: FILTER_LIST_K best (a, j) + the bound of the rest
-#define FILTER_LIST_K 8
+#define FILTER_LIST_K 4
 // rows_map == nullptr: every row of [lo, hi); else the nmap rows listed
 // (device count nmap_dev), whose A operands are gathered into imgA
 // (tc_image_bytes(nmap rounded up to 256, d) bytes)
