@@ -1,4 +1,5 @@
-"""Diagnostic: cProfile of run_pipeline at C1 (host overhead)."""
+"""Diagnostic: where a C1 run_pipeline spends its time (cProfile by
+cumulative time, 20 runs after warm-up, device input)."""
 import cProfile
 import pstats
 import sys
@@ -21,4 +22,4 @@ for _ in range(20):
 torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(25)
+st.sort_stats(sys.argv[1] if len(sys.argv) > 1 else "tottime").print_stats(30)
