@@ -262,7 +262,7 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
         }
         {
             const SymStage& s = ts.st[it & 1];
-#pragma unroll 4
+#pragma unroll 16
             for (int kk = 0; kk < SK; ++kk) {
                 const double2 a01 = *reinterpret_cast<const double2*>(&s.A[kk][rg * 4]);
                 const double2 a23 = *reinterpret_cast<const double2*>(&s.A[kk][rg * 4 + 2]);
