@@ -75,19 +75,58 @@ def workload(args):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed
-    region by ONE background nvidia-smi process (no forks inside the region)."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
+
+    NVML (pynvml) polled from a background thread every 20 ms -- short timed
+    regions (C1: a few ms per step) still get samples -- with one sample
+    taken at start(); if NVML is unavailable, one background nvidia-smi
+    process sampling every 200 ms (no forks inside the region)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.path = None
+        self.thread = None
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = 0.0
+
+    def _nvml_sample(self, nv, h):
+        self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        for name, attr in self.REASONS:
+            if bits & getattr(nv, attr, 0):
+                self.reasons.add(name)
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = [x.strip() for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
+            dev = self.index
+            if self.index < len(vis) and vis[self.index].isdigit():
+                dev = int(vis[self.index])   # NVML counts physical devices
+            h = nv.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._stop = threading.Event()
+            self._nvml_sample(nv, h)
+
+            def run():
+                while not self._stop.wait(0.02):
+                    self._nvml_sample(nv, h)
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         import tempfile
         fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
         os.close(fd)
@@ -100,6 +139,12 @@ class ClockSampler:
             self.proc = None
 
     def stop(self) -> dict:
+        if self.thread is not None:
+            self._stop.set()
+            self.thread.join(timeout=2)
+            sm = self.samples
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz or None,
+                    "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml 20 ms"}
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -123,7 +168,7 @@ class ClockSampler:
             except Exception:
                 continue
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi 200 ms"}
 
 
 def peaks():

@@ -92,9 +92,9 @@ def _fixture(name):
     return dg.load(path)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
 def test_pipeline_equals_oracle_full_size(name, pkg):
-    """BASELINE.json C2/C3/C4 at full size, every field bitwise vs the oracle."""
+    """BASELINE.json C1-C4 at full size, every field bitwise vs the oracle."""
     want = _fixture(name)
     m = want["meta"]
     pts, _ = pkg.generate_random(m["n"], m["d"], m["k"], m["seed"])

@@ -200,3 +200,19 @@ def test_tie_constructions_first_tie_round(oracle_mod):
         g = load(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz"))
         with pytest.raises(oracle_mod.TieError, match=f"round {rnd}$"):
             oracle_mod.run_pipeline_full(g["points"], int(g["k"]), root=int(g["root"]))
+
+
+def test_full_c1_fixture_is_the_reference_run():
+    """The C1 oracle digest (tests/golden/full_c1.json, bench.py's C1 parity
+    check) agrees with the reference's own C1 run (pipe_c1_seed0.npz)."""
+    import digest as dg
+    here = os.path.dirname(__file__)
+    want = dg.load(os.path.join(here, "golden", "full_c1.json"))
+    g = load(os.path.join(here, "golden", "pipe_c1_seed0.npz"))
+    assert want["sigma"] == dg.fbits(float(g["sigma"]))
+    assert want["miso"] == dg.fbits(float(g["miso"]))
+    assert want["iterations"] == int(g["iterations"])
+    assert want["labels"] == dg.ahash("labels", g["labels"])
+    assert want["parent"] == dg.ahash("parent", g["parent"])
+    assert want["omega"] == dg.ahash("omega", g["omega"])
+    assert want["trace_mid"] == [dg.fbits(m) for m in g["trace_mid"]]
