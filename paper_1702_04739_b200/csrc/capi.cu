@@ -345,10 +345,12 @@ struct isoc_mst {
     int64_t nblk;
     int lists_valid;
     int64_t filter_blocks_run, filter_blocks_total, filter_rows_refreshed;
+    int32_t* pin;   // page-locked copy of the counters (one per-round read-back)
 };
 
 static void mst_free(isoc_mst* h) {
     if (!h) return;
+    if (h->pin) cudaFreeHost(h->pin);
     void* ptrs[] = {h->img, h->Y, h->ny, h->rad, h->centre, h->rmax, h->comp, h->a1, h->a2, h->j1,
                     h->compB, h->cand_d, h->cand_j, h->cand_state, h->cand_tie, h->rescan_list,
                     h->counters, h->succ, h->succ2, h->eu, h->ev, h->ed, h->la, h->lb, h->lbo, h->lj,
@@ -481,9 +483,10 @@ int isoc_mst_round_local(isoc_mst* h, int use_nn, const int32_t* nn_j, const dou
                 CK(launch_list_refresh(h->a1, h->lbo, h->rad, h->comp, h->n, h->lo, h->hi, h->rmax, h->cd,
                                        h->cabs, h->compB, h->blk_flag, h->nblk, h->counters + 5,
                                        h->refresh_rows, st));
-                int32_t nf[2] = {0, 0};   // flagged blocks, rows
-                CK(cudaMemcpyAsync(nf, h->counters + 5, sizeof nf, cudaMemcpyDeviceToHost, st));
+                if (!h->pin) CK(cudaMallocHost((void**)&h->pin, 64));
+                CK(cudaMemcpyAsync(h->pin + 8, h->counters + 5, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
+                const int32_t nf[2] = {h->pin[8], h->pin[9]};   // flagged blocks, rows
                 h->filter_blocks_total += h->nblk;
                 h->filter_rows_refreshed += nf[1];
                 if (nf[1] > 0) {
@@ -524,9 +527,11 @@ int isoc_mst_round_finish(isoc_mst* h, const uint64_t* comp_min, const uint64_t*
                         ce, h->counters + 1, st));
     CK(launch_hook_contract(h->comp, h->n, cm, ce, h->succ, h->succ2, h->eu, h->ev, h->ed,
                             h->counters + 2, h->counters + 3, h->counters + 4, st));
-    int32_t c[8];
-    CK(cudaMemcpyAsync(c, h->counters, sizeof c, cudaMemcpyDeviceToHost, st));
+    if (!h->pin) CK(cudaMallocHost((void**)&h->pin, 64));
+    CK(cudaMemcpyAsync(h->pin, h->counters, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    int32_t c[8];
+    memcpy(c, h->pin, sizeof c);
     if (components) *components = c[4];
     if (ties) *ties = c[1];
     if (rescans) *rescans = c[0];
@@ -645,6 +650,7 @@ struct isoc_tree {
     int64_t* j_out;
     // batched speculative sweeps (isoc_decide_batch), allocated on first use
     int32_t bcap, bcap_small;
+    void* pin;   // page-locked staging for the per-sweep thresholds / counts (no blocking pageable copies)
     double *bom, *bp, *bthr;
     int8_t* bcode;
     int32_t *bexcl, *bscratch;
@@ -655,6 +661,7 @@ struct isoc_tree {
 };
 
 static void tree_free(isoc_tree* t) {
+    if (t && t->pin) cudaFreeHost(t->pin);
     if (!t) return;
     void* ptrs[] = {t->bfs, t->pos_of, t->parent_v, t->depth_v, t->child_id_v, t->pos_parent,
                     t->child_lo, t->child_cnt, t->parent_d, t->flow_v, t->level_off, t->omega_v,
@@ -867,11 +874,14 @@ int isoc_decide(isoc_tree* t, double N, int64_t k, int32_t slot, int64_t* j_host
         CK(dalloc(&t->spars[slot], k, t->st));
         t->spars_cap[slot] = k;
     }
+    if (!t->pin) CK(cudaMallocHost(&t->pin, 4096));
     CK(launch_decide(t->n, t->levels, t->level_off, t->max_width, t->f_pos, t->om_pos, t->p_pos,
                      t->child_lo, t->child_cnt, N, k, t->om_w, t->p_w, t->code[slot], t->excl,
                      t->spars[slot], t->scratch, t->j_out, st));
-    CK(cudaMemcpyAsync(j_host, t->j_out, 8, cudaMemcpyDeviceToHost, st));
+    int64_t* pj = static_cast<int64_t*>(t->pin);
+    CK(cudaMemcpyAsync(pj, t->j_out, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    *j_host = *pj;
     return ISOC_OK;
 }
 
@@ -909,12 +919,17 @@ int isoc_decide_batch(isoc_tree* t, const double* thresholds, int32_t count, int
             CK(dalloc(&t->bj, DECIDE_SMALL_MAX_BATCH, st));
             t->bcap_small = DECIDE_SMALL_MAX_BATCH;
         }
-        CK(cudaMemcpyAsync(t->bthr, thresholds, (size_t)count * 8, cudaMemcpyHostToDevice, st));
+        if (!t->pin) CK(cudaMallocHost(&t->pin, 4096));
+        double* pthr = static_cast<double*>(t->pin);
+        int64_t* pj = reinterpret_cast<int64_t*>(pthr + 64);
+        memcpy(pthr, thresholds, (size_t)count * 8);
+        CK(cudaMemcpyAsync(t->bthr, pthr, (size_t)count * 8, cudaMemcpyHostToDevice, st));
         CK(launch_decide_batch(t->n, t->levels, t->level_off, t->max_width, t->f_pos, t->om_pos, t->p_pos,
                                t->child_lo, t->child_cnt, t->bthr, count, k, nullptr, nullptr, nullptr,
                                nullptr, nullptr, t->bj, st));
-        CK(cudaMemcpyAsync(j_host, t->bj, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(pj, t->bj, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        memcpy(j_host, pj, (size_t)count * 8);
         return ISOC_OK;
     }
     for (int i = 0; i < count; ++i)

@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(512) decide_batch_kernel(DecideBatchArgs A) {
 // __syncthreads and shared-memory latencies instead of two grid barriers and
 // dependent global loads.  Same arithmetic, canonical order, k-th-cut stop
 // and fold order as decide_kernel (which is this with G = 1).
-constexpr int DS_THREADS = 32;
+constexpr int DS_THREADS = 512;   // staging threads; warp 0 sweeps
 
 size_t decide_small_smem(int64_t n, int64_t levels) {
     // f, om0, p0, om, p (8 B) + child_lo, child_cnt, excl (4 B) + code (1 B) + level_off
@@ -478,9 +478,12 @@ struct DecideSmallArgs {
 
 __global__ void __launch_bounds__(DS_THREADS, 1) decide_small_kernel(DecideSmallArgs A) {
     // one warp per threshold: MST levels are narrow (median width 6-71 at
-    // C1), so a level is a few shuffles and __syncwarp()s
+    // C1), so a level is a few shuffles and __syncwarp()s.  The CTA has
+    // DS_STAGE threads: all of them stage the tree into shared memory (the
+    // global loads overlap), then warp 0 alone sweeps.
     extern __shared__ __align__(16) unsigned char ds_raw[];
     const int lane = threadIdx.x;
+    const int nst = blockDim.x;
     const int64_t n = A.n, L = A.levels;
     double* f = reinterpret_cast<double*>(ds_raw);
     double* om0 = f + n;
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1) decide_small_kernel(DecideSmall
     int32_t* ccnt = clo + n;
     int32_t* excl = ccnt + n;
     int8_t* code = reinterpret_cast<int8_t*>(excl + n);
-    for (int64_t q = lane; q < n; q += 32) {
+    for (int64_t q = lane; q < n; q += nst) {
         f[q] = A.f_pos[q];
         om0[q] = A.om0[q];
         p0[q] = A.p0[q];
@@ -500,8 +503,9 @@ __global__ void __launch_bounds__(DS_THREADS, 1) decide_small_kernel(DecideSmall
         ccnt[q] = A.child_cnt[q];
         code[q] = 0;
     }
-    for (int64_t q = lane; q <= L; q += 32) loff[q] = A.level_off[q];
-    __syncwarp();
+    for (int64_t q = lane; q <= L; q += nst) loff[q] = A.level_off[q];
+    __syncthreads();
+    if (lane >= 32) return;
     const double thr = A.thr[blockIdx.x];
     const bool witness = A.code != nullptr;
     int64_t j = 0, stop_lo = 0;

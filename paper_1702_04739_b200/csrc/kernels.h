@@ -32,6 +32,10 @@ cudaError_t launch_transpose_pad(const double* X, int64_t n, int d, int64_t np, 
 // sigma_sym.cu
 bool sigma_sym_applicable(int64_t n, int64_t lo, int64_t hi, int want_p);
 int device_sm_count();   // SMs of the current device (cached per device)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `bytes` exceeds
+// what was last set for this kernel on this device (the call costs tens of
+// microseconds; small-tree kernels launch per bisection batch)
+cudaError_t ensure_max_dyn_smem(const void* func, size_t bytes);
 int passes_mode();       // ISOC_PASSES test hook: 0 auto, 1 "sym", 2 "rows"
 cudaError_t launch_sigma_sym(const double* X, int64_t n, int d, double* row_vals, uint64_t* row_ids,
                              int32_t* row_cnt, int32_t* flags, int32_t* nn_j, double* nn_d,

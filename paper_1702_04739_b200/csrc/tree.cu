@@ -419,18 +419,22 @@ cudaError_t launch_children_from_parent(const int64_t* parent, const int64_t* ch
 // (children in adjacency order, i.e. Prim's (d, id) rank for the MST).
 constexpr int64_t BFS_SMALL_N = 8192;
 
-__global__ void __launch_bounds__(32, 1) bfs_small_kernel(BfsArgs A) {
+__global__ void __launch_bounds__(512, 1) bfs_small_kernel(BfsArgs A) {
+    // all 512 threads stage the adjacency (overlapping the global loads),
+    // then warp 0 alone walks the levels
     extern __shared__ __align__(16) unsigned char bs_raw[];
     const int lane = threadIdx.x;
+    const int nst = blockDim.x;
     const int64_t n = A.n;
     int32_t* off = reinterpret_cast<int32_t*>(bs_raw);
     const int64_t m = A.off[n];
     int32_t* adj = off + n + 1;
     int32_t* bfs = adj + m;
     int32_t* par = bfs + n;
-    for (int64_t q = lane; q <= n; q += 32) off[q] = A.off[q];
-    for (int64_t q = lane; q < m; q += 32) adj[q] = A.adj[q];
-    __syncwarp();
+    for (int64_t q = lane; q <= n; q += nst) off[q] = A.off[q];
+    for (int64_t q = lane; q < m; q += nst) adj[q] = A.adj[q];
+    __syncthreads();
+    if (lane >= 32) return;
     if (lane == 0) {
         bfs[0] = (int32_t)A.root;
         par[A.root] = -1;
@@ -537,11 +541,10 @@ cudaError_t launch_bfs(int64_t n, int64_t root, int undirected, const int32_t* o
         // off (n+1) + adj (<= 2n) + bfs (n) + parents (n), int32: the adjacency
         // length is read on the device, so size for the undirected maximum
         const size_t smem = (size_t)(n + 1 + 2 * n + 2 * n) * sizeof(int32_t);
-        cudaError_t e = cudaFuncSetAttribute(bfs_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = ensure_max_dyn_smem((const void*)bfs_small_kernel, smem);
         if (e != cudaSuccess) return e;
         const int pid = prof_begin(PK_BFS, st);
-        bfs_small_kernel<<<1, 32, smem, st>>>(A);
+        bfs_small_kernel<<<1, 512, smem, st>>>(A);
         prof_end(pid, st);
         note_launch();
         return cudaGetLastError();

@@ -92,9 +92,10 @@ def _fixture(name):
     return dg.load(path)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c2_seed1", "c3_seed1", "c4_seed1"])
 def test_pipeline_equals_oracle_full_size(name, pkg):
-    """BASELINE.json C1-C4 at full size, every field bitwise vs the oracle."""
+    """BASELINE.json C1-C4 at full size (seed 0, and seed 1 -- SURVEY 8(d)'s
+    second seed), every field bitwise vs the oracle."""
     want = _fixture(name)
     m = want["meta"]
     pts, _ = pkg.generate_random(m["n"], m["d"], m["k"], m["seed"])

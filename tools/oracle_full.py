@@ -5,7 +5,7 @@ operation order, vectorised across pairs, certified-unique MST) on the
 BASELINE.json configs and writes tests/golden/full_<name>.json digests
 (tests/digest.py).  Long-running at C3 (about an hour on 8 cores): run in the
 background in the CPU container.
-    python tools/oracle_full.py c3|c4|c5|<n> <d> <k> [seed]
+    python tools/oracle_full.py c3|c4|c5|<n> <d> <k> [seed]      (c1-c4: --seed S for another seed)
 For n <= 46,340 `--check` compares against the reference digests
 (tests/golden/large_*.json) instead of writing.
 """
@@ -76,12 +76,20 @@ def main(argv):
     check = "--check" in argv
     argv = [a for a in argv if a != "--check"]
     name = argv[0]
+    seed_override = None
+    if "--seed" in argv:
+        i = argv.index("--seed")
+        seed_override = int(argv[i + 1])
+        del argv[i:i + 2]
     if name == "c5":
         n, k, seed = C5
         dig = tree_digest(n, k, seed)
     else:
         if name in CONFIGS:
             n, d, k, seed = CONFIGS[name]
+            if seed_override is not None:
+                seed = seed_override
+                name = f"{name}_seed{seed}"
         else:
             n, d, k = (int(a) for a in argv[:3])
             seed = int(argv[3]) if len(argv) > 3 else 0
