@@ -10,9 +10,10 @@ rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[0]
+units = dict(zip(hdr, rows[1]))
 sel = [int(a) for a in sys.argv[2:]] or list(range(len(rows) - 2))
 KEYS = [
-    ("gpu__time_duration.sum", "duration (ns)"),
+    ("gpu__time_duration.sum", "duration"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active %"),
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 inst executed % of peak"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active %"),
@@ -37,7 +38,7 @@ for i in sel:
     print(f"== kernel {i}: {d.get('Kernel Name', '')[:90]}")
     for k, label in KEYS:
         if k in d:
-            print(f"  {label:34s} {d[k]}")
+            print(f"  {label:34s} {d[k]} {units.get(k, '')}")
     st = []
     for k, v in d.items():
         if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
