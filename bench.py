@@ -403,8 +403,9 @@ def tree_phase_bench(args):
         roofline = {"kernel": "decide", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": 1.721e9,
                     "traffic_unit": "bytes per launch (mean over the 78 sweeps of one step)",
-                    "traffic_source": "profiles/round1_ncu_launches_decide_c5.csv (dram__bytes_read.sum + "
-                                      "dram__bytes_write.sum per decide_kernel launch; mean 0.91 ms, 1.90 TB/s)",
+                    "traffic_source": "profiles/round2_ncu_launches_decide_c5.csv (dram__bytes_read.sum + "
+                                      "dram__bytes_write.sum per decide_kernel launch, 156 launches = 2 steps; "
+                                      "mean 0.914 ms, 1.72 GB, 1.88 TB/s)",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                     "note": "algorithmic 45 B/vertex x n per sweep (SURVEY 8(d)); sweeps stop at the k-th cut, "
                             "so the measured DRAM traffic is lower; level-synchronous (grid barriers per level), "
