@@ -70,13 +70,15 @@ def _check(got: dict, want: dict):
     assert bad == [], {k: (got.get(k), want.get(k)) for k in bad[:3]}
 
 
-@pytest.mark.parametrize("name", ["n16000_d64_k20", "n32000_d16_k10", "n46340_d64_k20"])
+@pytest.mark.parametrize("name", ["n16000_d64_k20", "n32000_d16_k10", "n46340_d64_k20",
+                                  "n20000_d16_k8_sigma3_root777", "n12000_d32_k12_alpha0.5"])
 def test_pipeline_equals_reference_large(name, pkg):
-    """run_pipeline == the reference's own run at up to its dense cap."""
+    """run_pipeline == the reference's own run at up to its dense cap, with
+    the default arguments and with an explicit sigma + root and alpha > 0."""
     want = dg.load(os.path.join(GOLDEN, f"large_{name}.json"))
     m = want["meta"]
     pts, _ = pkg.generate_random(m["n"], m["d"], m["k"], m["seed"])
-    run = pkg.run_pipeline(pts, m["k"])
+    run = pkg.run_pipeline(pts, m["k"], sigma=m["sigma_arg"], alpha=m["alpha"], root=m["root"])
     got = _pipeline_digest(run)
     got["total_distance"] = dg.fbits(_tree_weight(pkg, pts, run.tree))
     _check(got, want)

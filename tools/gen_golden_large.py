@@ -22,11 +22,14 @@ PIN = "AVX512F AVX512CD AVX512_SKX AVX512_CLX AVX512_CNL AVX512_ICL AVX512_SPR"
 ROOT = Path(__file__).resolve().parents[1]
 OUT = ROOT / "tests" / "golden"
 
-# (name, n, d, k, seed)
+# (name, n, d, k, seed[, sigma, alpha, root])
 CASES = [
     ("n16000_d64_k20", 16000, 64, 20, 0),
     ("n32000_d16_k10", 32000, 16, 10, 0),
     ("n46340_d64_k20", 46340, 64, 20, 0),
+    # the boundary's other arguments at scale: explicit sigma + root, alpha > 0
+    ("n20000_d16_k8_sigma3_root777", 20000, 16, 8, 2, 3.0, 0.0, 777),
+    ("n12000_d32_k12_alpha0.5", 12000, 32, 12, 3, "auto", 0.5, 0),
 ]
 
 
@@ -42,7 +45,9 @@ def main() -> None:
 
     only = set(sys.argv[1:]) or None
     workers = os.cpu_count()
-    for name, n, d, k, seed in CASES:
+    for case in CASES:
+        name, n, d, k, seed = case[:5]
+        sigma_arg, alpha, root = (case[5], case[6], case[7]) if len(case) > 5 else ("auto", 0.0, 0)
         if only and name not in only:
             continue
         pts, _ = ic.generate_random(n, d, k, seed)
@@ -51,13 +56,13 @@ def main() -> None:
         dist = ic.distance_matrix(pts, workers=workers)
         t["distance_matrix"] = time.perf_counter() - t0
         t0 = time.perf_counter()
-        sigma = ic.auto_sigma(dist)
+        sigma = ic.auto_sigma(dist) if sigma_arg == "auto" else float(sigma_arg)
         t["auto_sigma"] = time.perf_counter() - t0
         t0 = time.perf_counter()
-        tree = ic.prim_mst(dist, sigma, 0)
+        tree = ic.prim_mst(dist, sigma, root)
         t["prim_mst"] = time.perf_counter() - t0
         t0 = time.perf_counter()
-        w = ic.node_weights(dist, sigma, 0.0, workers=workers)
+        w = ic.node_weights(dist, sigma, alpha, workers=workers)
         ext = ic.extrema(tree, w)
         t["node_weights_extrema"] = time.perf_counter() - t0
         t0 = time.perf_counter()
@@ -74,7 +79,7 @@ def main() -> None:
         dig["dsum"] = dg.fbits(dsum)
         dig["meta"] = {
             "source": "reference isoclust run_pipeline stages (pinned numpy), tools/gen_golden_large.py",
-            "n": n, "d": d, "k": k, "seed": seed, "sigma_arg": "auto", "alpha": 0.0, "root": 0,
+            "n": n, "d": d, "k": k, "seed": seed, "sigma_arg": sigma_arg, "alpha": alpha, "root": root,
             "engine": "par", "workers": workers, "stage_seconds": {a: round(b, 3) for a, b in t.items()},
             "numpy": np.__version__, "cpu_count": os.cpu_count(),
         }
