@@ -43,3 +43,26 @@ def test_ladder_fit_is_exact_on_model_data():
     assert abs(fit["extrapolated_s"]["sigma"] - 2000.0) < 1e-6
     assert abs(fit["extrapolated_s"]["partition"] - 0.5) < 1e-9
     assert abs(fit["total_s"] - (2000 + 3000 + 1000 + 0.5)) < 1e-6
+
+
+def test_fixture_parity_accepts_the_oracle_run_and_rejects_a_perturbed_one(oracle_mod):
+    """bench.fixture_parity (the bench's post-timing parity check) on the C1
+    oracle run: fixture-match; with one label changed: MISMATCH."""
+    import types
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+
+    pts, _ = oracle_mod.generate_random(2000, 2, 3, 0)
+    out = oracle_mod.run_pipeline(pts, 3)
+    e = out.extrema
+    run = types.SimpleNamespace(
+        result=out.result, sigma=out.sigma, tree=out.tree, extrema=e,
+        omega_host=lambda: out.omega, p_host=lambda: out.p)
+    got = bench.fixture_parity("c1", 2000, 2, 3, run)
+    assert got["status"] == "fixture-match" and got["fields_compared"] >= 20, got
+    bad = out.result.labels.copy()
+    bad[0] = (bad[0] % 3) + 1
+    run.result = types.SimpleNamespace(**{**out.result.__dict__, "labels": bad})
+    got = bench.fixture_parity("c1", 2000, 2, 3, run)
+    assert got["status"] == "MISMATCH" and "labels" in got["differs"]
