@@ -439,25 +439,67 @@ __global__ void rescan_kernel(const double* __restrict__ X, int64_t n, int d,
 }
 
 // Tiled exact rescan: work item (group of RR rescan rows, chunk of RCW
-// columns); each column tile of 128 points is read once for all RR rows.
-// Per (row, chunk) the lexicographic (d, j) minimum over other-component
-// columns and the second-smallest value (tie flag) go to scratch; the reduce
-// kernel folds the chunks in column order.
+// columns); each column tile of RT points is read once for all RR rows.
+// Global -> shared through a cp.async double buffer (8-byte copies transpose
+// row-major X into k-major tiles; out-of-range rows, columns and k zero-fill,
+// and a zero pair adds an exact (0-0)^2 = 0).  Thread (ty, tx) owns rows
+// 4ty..4ty+3 (two broadcast LDS.128) and columns 2tx + 64j + {0,1} (four
+// LDS.128): 6 shared loads per 96 fp64 ops.  Per (row, chunk) the
+// lexicographic (d, j) minimum over other-component columns and the
+// second-smallest value (tie flag) go to scratch; the reduce kernel folds the
+// chunks in column order.
 constexpr int RR = 32;
+constexpr int RT = 256;
 constexpr int RCW = 32768;
 constexpr int RKC = 16;
+constexpr int RBS = RT + 2;   // B row stride (doubles): 16-byte aligned rows
+struct RescanStage {
+    double A[RKC][RR];
+    double B[RKC][RBS];
+};
+constexpr size_t RESCAN_SMEM = 2 * sizeof(RescanStage);
 
-__global__ void __launch_bounds__(256, 2)
+// Column chunking from the device-side row count: at least the RCW-wide
+// chunks, narrower (down to one RT tile) when few row groups would leave SMs
+// idle -- (row group, chunk) items fill the SMs about eight times over.
+// Partials live at q * nchunks + c; cnt * nchunks <= rescan_capacity(rows).
+struct RescanChunks {
+    int64_t cw, nchunks;
+};
+__host__ __device__ __forceinline__ RescanChunks rescan_chunks(int64_t cnt, int64_t n, int sms) {
+    const int64_t ngroups = (cnt + RR - 1) / RR;
+    const int64_t nc0 = (n + RCW - 1) / RCW, ncmax = (n + RT - 1) / RT;
+    int64_t want = ngroups > 0 ? (8 * (int64_t)sms + ngroups - 1) / ngroups : 1;
+    if (want > ncmax) want = ncmax;
+    const int64_t nch = want > nc0 ? want : nc0;
+    int64_t cw = (n + nch - 1) / nch;
+    cw = (cw + RT - 1) / RT * RT;
+    if (cw < RT) cw = RT;
+    return {cw, (n + cw - 1) / cw};
+}
+static int64_t rescan_capacity(int64_t rows, int64_t n, int sms) {
+    return rows * ((n + RCW - 1) / RCW + 1) + (int64_t)RR * (8 * (int64_t)sms + 1);
+}
+
+__device__ __forceinline__ void rcp8(void* dst, const void* src, bool ok) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(ok ? 8 : 0));
+}
+
+__global__ void __launch_bounds__(256, 1)
 rescan_tile_kernel(const double* __restrict__ X, int64_t n, int d, const int32_t* __restrict__ comp,
                    const int32_t* __restrict__ rescan_list, const int32_t* __restrict__ rescan_count,
-                   int64_t nchunks, double* __restrict__ pm1, double* __restrict__ pm2,
+                   int sms, double* __restrict__ pm1, double* __restrict__ pm2,
                    int32_t* __restrict__ pj) {
-    __shared__ double As[2][RKC][RR];
-    __shared__ double Bs[2][RKC][129];
+    extern __shared__ __align__(16) unsigned char rsm[];
+    RescanStage* stg = reinterpret_cast<RescanStage*>(rsm);
     __shared__ int32_t crow[RR];
+    __shared__ int32_t grow[RR];
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const int64_t cnt = *rescan_count;
     const int64_t ngroups = (cnt + RR - 1) / RR;
+    const RescanChunks ch = rescan_chunks(cnt, n, sms);
+    const int64_t cw = ch.cw, nchunks = ch.nchunks;
     const int64_t items = ngroups * nchunks;
     const int nkc = (d + RKC - 1) / RKC;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
@@ -465,80 +507,81 @@ rescan_tile_kernel(const double* __restrict__ X, int64_t n, int d, const int32_t
         __syncthreads();
         if (tid < RR) {
             const int64_t q = g * RR + tid;
-            crow[tid] = q < cnt ? comp[rescan_list[q]] : INT32_MIN;
+            const int32_t r = q < cnt ? rescan_list[q] : -1;
+            grow[tid] = r;
+            crow[tid] = r >= 0 ? comp[r] : INT32_MIN;
         }
+        __syncthreads();
         double m1[4], m2[4];
         int32_t j1[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) { m1[i] = INFINITY; m2[i] = INFINITY; j1[i] = INT32_MAX; }
-        const int64_t cend = ((c + 1) * RCW < n) ? (c + 1) * RCW : n;
-        for (int64_t t0 = c * RCW; t0 < cend; t0 += 128) {
-            double acc[4][4];
+        const int64_t cend = ((c + 1) * cw < n) ? (c + 1) * cw : n;
+        for (int64_t t0 = c * cw; t0 < cend; t0 += RT) {
+            double acc[4][8];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-            // k chunks through registers into a double-buffered tile: the
-            // global loads of chunk kc+1 are in flight while chunk kc computes
-            double ra[2], rb[8];
-            auto gload = [&](int k0) {
+                for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+            auto issue = [&](int kc, RescanStage& S) {
+                const int k0 = kc * RKC;
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int idx = tid + 256 * e;
                     const int r = idx / RKC, kk = idx % RKC;
-                    const int64_t q = g * RR + r;
-                    ra[e] = (q < cnt && k0 + kk < d) ? X[(int64_t)rescan_list[q] * d + k0 + kk] : 0.0;
+                    const int32_t gr = grow[r];
+                    const bool ok = gr >= 0 && k0 + kk < d;
+                    rcp8(&S.A[kk][r], ok ? X + (int64_t)gr * d + k0 + kk : X, ok);
                 }
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
+                for (int e = 0; e < 16; ++e) {
                     const int idx = tid + 256 * e;
                     const int j = idx / RKC, kk = idx % RKC;
                     const int64_t col = t0 + j;
-                    rb[e] = (col < n && k0 + kk < d) ? X[col * d + k0 + kk] : 0.0;
+                    const bool ok = col < n && k0 + kk < d;
+                    rcp8(&S.B[kk][j], ok ? X + col * d + k0 + kk : X, ok);
                 }
+                asm volatile("cp.async.commit_group;\n" ::);
             };
-            auto sstore = [&](int buf) {
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int idx = tid + 256 * e;
-                    As[buf][idx % RKC][idx / RKC] = ra[e];
-                }
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int idx = tid + 256 * e;
-                    Bs[buf][idx % RKC][idx / RKC] = rb[e];
-                }
-            };
-            gload(0);
-            sstore(0);
-            __syncthreads();
+            issue(0, stg[0]);
             for (int kc = 0; kc < nkc; ++kc) {
-                if (kc + 1 < nkc) gload((kc + 1) * RKC);
-                const int buf = kc & 1;
+                if (kc + 1 < nkc) {
+                    issue(kc + 1, stg[(kc + 1) & 1]);
+                    asm volatile("cp.async.wait_group 1;\n" ::);
+                } else {
+                    asm volatile("cp.async.wait_group 0;\n" ::);
+                }
+                __syncthreads();
+                const RescanStage& S = stg[kc & 1];
 #pragma unroll
                 for (int kk = 0; kk < RKC; ++kk) {
-                    double a[4], bb[4];
+                    const double2 a01 = *reinterpret_cast<const double2*>(&S.A[kk][4 * ty]);
+                    const double2 a23 = *reinterpret_cast<const double2*>(&S.A[kk][4 * ty + 2]);
+                    const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+                    double bb[8];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][ty + 8 * i];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) bb[j] = Bs[buf][kk][tx + 32 * j];
+                    for (int j = 0; j < 4; ++j) {
+                        const double2 v = *reinterpret_cast<const double2*>(&S.B[kk][2 * tx + 64 * j]);
+                        bb[2 * j] = v.x;
+                        bb[2 * j + 1] = v.y;
+                    }
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) acc[i][j] = exact_sq_step(acc[i][j], a[i], bb[j]);
+                        for (int j = 0; j < 8; ++j) acc[i][j] = exact_sq_step(acc[i][j], a[i], bb[j]);
                 }
-                if (kc + 1 < nkc) sstore((kc + 1) & 1);
                 __syncthreads();
             }
-            // zero-padded k beyond d adds exact zeros: (0-0)^2 = 0
+            // columns in increasing order per thread: a strict < keeps the
+            // smallest column among equal values
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int64_t col = t0 + tx + 32 * j;
+            for (int j = 0; j < 8; ++j) {
+                const int64_t col = t0 + 2 * tx + 64 * (j >> 1) + (j & 1);
                 if (col >= n) continue;
                 const int32_t cc = comp[col];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    if (cc == crow[ty + 8 * i]) continue;
+                    if (cc == crow[4 * ty + i]) continue;
                     const double v = __dsqrt_rn(acc[i][j]);
                     const bool lt = v < m1[i];
                     const double cand = lt ? m1[i] : v;
@@ -563,7 +606,7 @@ rescan_tile_kernel(const double* __restrict__ X, int64_t n, int d, const int32_t
                 m1[i] = other_first ? om1 : m1[i];
                 j1[i] = other_first ? oj : j1[i];
             }
-            const int64_t q = g * RR + ty + 8 * i;
+            const int64_t q = g * RR + 4 * ty + i;
             if (tx == 0 && q < cnt) {
                 pm1[q * nchunks + c] = m1[i];
                 pm2[q * nchunks + c] = m2[i];
@@ -575,11 +618,12 @@ rescan_tile_kernel(const double* __restrict__ X, int64_t n, int d, const int32_t
 
 __global__ void rescan_reduce_kernel(const int32_t* __restrict__ rescan_list,
                                      const int32_t* __restrict__ rescan_count, int64_t lo,
-                                     int64_t nchunks, const double* __restrict__ pm1,
+                                     int64_t n, int sms, const double* __restrict__ pm1,
                                      const double* __restrict__ pm2, const int32_t* __restrict__ pj,
                                      double* __restrict__ cand_d, int32_t* __restrict__ cand_j,
                                      int8_t* __restrict__ cand_tie) {
     const int64_t cnt = *rescan_count;
+    const int64_t nchunks = rescan_chunks(cnt, n, sms).nchunks;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt;
          q += (int64_t)gridDim.x * blockDim.x) {
         double m1 = INFINITY, m2 = INFINITY;
@@ -599,6 +643,35 @@ __global__ void rescan_reduce_kernel(const int32_t* __restrict__ rescan_list,
         cand_j[i - lo] = j1 == INT32_MAX ? -1 : j1;
         cand_tie[i - lo] = (int8_t)(m2 == m1);
     }
+}
+
+// Exact rescans of the rows in rescan_list (count on the device): tiles ->
+// per-chunk partials -> fold, into cand_* (indexed by row - lo).
+static cudaError_t launch_rescan(const double* X, int64_t n, int d, const int32_t* comp, int64_t lo,
+                                 int64_t rows, const int32_t* rescan_list, const int32_t* rescan_count,
+                                 double* cand_d, int32_t* cand_j, int8_t* cand_tie, cudaStream_t st) {
+    const int sms = device_sm_count();
+    cudaError_t e = ensure_max_dyn_smem((const void*)rescan_tile_kernel, RESCAN_SMEM);
+    if (e != cudaSuccess) return e;
+    const size_t cap = (size_t)rescan_capacity(rows, n, sms);
+    double *pm1 = nullptr, *pm2 = nullptr;
+    int32_t* pj = nullptr;
+    e = cudaMallocAsync((void**)&pm1, cap * 8, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMallocAsync((void**)&pm2, cap * 8, st);
+    if (e != cudaSuccess) { cudaFreeAsync(pm1, st); return e; }
+    e = cudaMallocAsync((void**)&pj, cap * 4, st);
+    if (e != cudaSuccess) { cudaFreeAsync(pm1, st); cudaFreeAsync(pm2, st); return e; }
+    const int pid = prof_begin(PK_RESCAN, st);
+    rescan_tile_kernel<<<sms, 256, RESCAN_SMEM, st>>>(X, n, d, comp, rescan_list, rescan_count, sms, pm1, pm2,
+                                                      pj);
+    rescan_reduce_kernel<<<sms, 256, 0, st>>>(rescan_list, rescan_count, lo, n, sms, pm1, pm2, pj, cand_d,
+                                              cand_j, cand_tie);
+    prof_end(pid, st);
+    cudaFreeAsync(pm1, st);
+    cudaFreeAsync(pm2, st);
+    cudaFreeAsync(pj, st);
+    return cudaGetLastError();
 }
 
 // Round 1 from the fused exact nearest neighbours: every row is a candidate.
@@ -779,26 +852,9 @@ cudaError_t launch_boruvka_select(const double* X, int64_t n, int d, const float
     candidate_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(X, d, a1, j1, a2, rad, comp, lo, hi,
                                                              rmax_bits, cd, cabs, compB, cand_d, cand_j,
                                                              cand_state, rescan_list, rescan_count);
-    const int64_t nchunks = (n + RCW - 1) / RCW;
-    double *pm1 = nullptr, *pm2 = nullptr;
-    int32_t* pj = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&pm1, (size_t)rows * nchunks * 8, st);
-    if (e != cudaSuccess) return e;
-    e = cudaMallocAsync((void**)&pm2, (size_t)rows * nchunks * 8, st);
-    if (e != cudaSuccess) return e;
-    e = cudaMallocAsync((void**)&pj, (size_t)rows * nchunks * 4, st);
-    if (e != cudaSuccess) return e;
-    const int pid = prof_begin(PK_RESCAN, st);
-    rescan_tile_kernel<<<148 * 3, 256, 0, st>>>(X, n, d, comp, rescan_list, rescan_count, nchunks, pm1,
-                                                pm2, pj);
-    rescan_reduce_kernel<<<148, 256, 0, st>>>(rescan_list, rescan_count, lo, nchunks, pm1, pm2, pj,
-                                              cand_d, cand_j, cand_tie);
-    prof_end(pid, st);
+    cudaError_t e = launch_rescan(X, n, d, comp, lo, rows, rescan_list, rescan_count, cand_d, cand_j, cand_tie, st);
     note_launch(4);
-    cudaFreeAsync(pm1, st);
-    cudaFreeAsync(pm2, st);
-    cudaFreeAsync(pj, st);
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_list_select(const float* la, const int32_t* lj, const float* lb, const int32_t* comp,
@@ -846,25 +902,9 @@ cudaError_t launch_boruvka_exact_all(const double* X, int64_t n, int d, const in
     if (rows <= 0) return cudaSuccess;
     cudaMemsetAsync(cand_tie, 0, (size_t)rows, st);
     all_rows_rescan_kernel<<<blocks_for(rows, 256), 256, 0, st>>>(lo, hi, cand_state, rescan_list, rescan_count);
-    const int64_t nchunks = (n + RCW - 1) / RCW;
-    double *pm1 = nullptr, *pm2 = nullptr;
-    int32_t* pj = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&pm1, (size_t)rows * nchunks * 8, st);
-    if (e != cudaSuccess) return e;
-    e = cudaMallocAsync((void**)&pm2, (size_t)rows * nchunks * 8, st);
-    if (e != cudaSuccess) { cudaFreeAsync(pm1, st); return e; }
-    e = cudaMallocAsync((void**)&pj, (size_t)rows * nchunks * 4, st);
-    if (e != cudaSuccess) { cudaFreeAsync(pm1, st); cudaFreeAsync(pm2, st); return e; }
-    const int pid = prof_begin(PK_RESCAN, st);
-    rescan_tile_kernel<<<148 * 3, 256, 0, st>>>(X, n, d, comp, rescan_list, rescan_count, nchunks, pm1, pm2, pj);
-    rescan_reduce_kernel<<<148, 256, 0, st>>>(rescan_list, rescan_count, lo, nchunks, pm1, pm2, pj, cand_d,
-                                              cand_j, cand_tie);
-    prof_end(pid, st);
+    cudaError_t e = launch_rescan(X, n, d, comp, lo, rows, rescan_list, rescan_count, cand_d, cand_j, cand_tie, st);
     note_launch(3);
-    cudaFreeAsync(pm1, st);
-    cudaFreeAsync(pm2, st);
-    cudaFreeAsync(pj, st);
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_nn_candidates(const int32_t* nn_j, const double* nn_d, const int8_t* nn_tie,
