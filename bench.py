@@ -614,19 +614,29 @@ def main():
     # mul/add), so their ceiling is the DADD/DMUL issue rate = half the
     # measured DFMA flop rate
     fp64_op_peak = fp64_peak.value / 2.0
-    # pairs the exact passes actually evaluate (one GPU: symmetric super-tiles
-    # of 1024; sigma adds 128-wide leaf strips beyond each super-block)
+    # pairs the exact passes actually evaluate (one GPU: symmetric super-tiles;
+    # sigma computes a 128-column leaf strip only for the row chains of each
+    # wave's last column block -- every other straddling leaf is finished by
+    # the merge from dumped distances)
     executed_pairs = {}
     if world == 1:
-        # sigma: 2048-wide super-blocks of 16 x 16 tiles of 128 (+ a strip of 16
-        # tiles per direction); omega: 1024-wide super-blocks, no strip
+        # sigma: 2048-wide super-blocks of 16 x 16 tiles of 128, waves planned
+        # as launch_sigma_sym_range does (40 GB of 1364-byte slots, >= 8
+        # blocks); omega: 1024-wide super-blocks, no strip
         sb, nt = 2048, 16
         nbs = -(-n // sb)
-        tiles = 0
-        for J in range(nbs):
-            ext = 1 if J + 1 < nbs else 0
-            tiles += J * (nt * nt + nt * ext + nt) + (nt * nt + nt * ext) if n >= 2048 else 0
         if n >= 2048:
+            budget = (40 << 30) // (32 * 8 + 20 + 136 * 8)
+            last = set()
+            w0 = 0
+            while w0 < nbs:
+                yg = 8
+                while w0 + yg < nbs and (yg + 1) * (n + sb * (w0 + yg + 1)) <= budget:
+                    yg += 1
+                w1 = min(w0 + yg, nbs)
+                last.add(w1 - 1)
+                w0 = w1
+            tiles = sum((J + 1) * nt * (nt + (1 if (J in last and J + 1 < nbs) else 0)) for J in range(nbs))
             executed_pairs["sigma_pass"] = tiles * 128 * 128
         nbo = -(-n // 1024)
         executed_pairs["omega_pass"] = nbo * (nbo + 1) // 2 * 1024 * 1024
@@ -672,8 +682,8 @@ def main():
             roofline["executed"] = kernels[dom]["executed"]
             roofline["note"] = ("algorithmic = 3*d fp64 flops x n(n-1)/2 unordered pairs (d_ij == d_ji "
                                 "bitwise, so one evaluation per pair is the minimum work); 'executed' adds "
-                                "the pairs the tiling really evaluates (diagonal tiles, 128-column leaf "
-                                "strip) -- the FP64 pipe's view; SURVEY 8(d)'s ordered-pair count (n^2) "
+                                "the pairs the tiling really evaluates (diagonal tiles, the 128-column "
+                                "leaf strip of each wave's last block) -- the FP64 pipe's view; SURVEY 8(d)'s ordered-pair count (n^2) "
                                 "would read 2x 'achieved'")
 
     if roofline is None and dom == "decide":

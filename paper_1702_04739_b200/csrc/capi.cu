@@ -87,6 +87,37 @@ cudaError_t aalloc(T** p, size_t count, cudaStream_t st) {
     return cudaMallocAsync(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), st);
 }
 
+// Per-thread scratch arena for the partition phase (batched sweeps, the
+// witness): its buffers outlive the tree handles, so repeated pipeline runs
+// allocate nothing there (a pool allocation inside the bisection loop was
+// seen to stall the host for up to ~0.3 s).  Growth frees the old buffer in
+// stream order; every user synchronizes its stream before returning, so a
+// buffer is idle whenever another handle picks it up.
+enum ArenaSlot { AR_BOM, AR_BP, AR_BCODE, AR_BEXCL, AR_BSCRATCH, AR_BTHR, AR_BJ, AR_CUT, AR_ETA, AR_LAB,
+                 AR_LAB32, AR_WORK, AR_SUMS, AR_MISO, AR_CWORK, AR_COUNT };
+template <typename T>
+cudaError_t arena(ArenaSlot slot, T** p, size_t count, cudaStream_t st) {
+    struct Buf { void* p = nullptr; size_t bytes = 0; int dev = -1; };
+    static thread_local Buf bufs[AR_COUNT];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const size_t bytes = (count ? count : 1) * sizeof(T);
+    Buf& b = bufs[slot];
+    if (b.dev != dev || b.bytes < bytes) {
+        if (b.p && b.dev == dev) cudaFreeAsync(b.p, st);
+        b.p = nullptr;
+        b.bytes = 0;
+        ensure_pool();
+        e = cudaMallocAsync(&b.p, bytes, st);
+        if (e != cudaSuccess) return e;
+        b.bytes = bytes;
+        b.dev = dev;
+    }
+    *p = static_cast<T*>(b.p);
+    return cudaSuccess;
+}
+
 __global__ void scale_kernel(double* v, int64_t m, double a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) v[i] = __dmul_rn(a, v[i]);
@@ -649,7 +680,6 @@ struct isoc_tree {
     int32_t *excl, *scratch;
     int64_t* j_out;
     // batched speculative sweeps (isoc_decide_batch), allocated on first use
-    int32_t bcap, bcap_small;
     void* pin;   // page-locked staging for the per-sweep thresholds / counts (no blocking pageable copies)
     double *bom, *bp, *bthr;
     int8_t* bcode;
@@ -666,8 +696,7 @@ static void tree_free(isoc_tree* t) {
     void* ptrs[] = {t->bfs, t->pos_of, t->parent_v, t->depth_v, t->child_id_v, t->pos_parent,
                     t->child_lo, t->child_cnt, t->parent_d, t->flow_v, t->level_off, t->omega_v,
                     t->p_v, t->f_pos, t->om_pos, t->p_pos, t->om_w, t->p_w, t->code[0], t->code[1],
-                    t->spars[0], t->spars[1], t->excl, t->scratch, t->j_out, t->bom, t->bp,
-                    t->bthr, t->bcode, t->bexcl, t->bscratch, t->bj};
+                    t->spars[0], t->spars[1], t->excl, t->scratch, t->j_out};
     for (void* p : ptrs)
         if (p) cudaFreeAsync(p, t->st);
     if (t->side) {
@@ -909,16 +938,8 @@ int isoc_decide_batch(isoc_tree* t, const double* thresholds, int32_t count, int
     if (decide_small_fits(t->n, t->levels, &smem_small)) {
         // one warp per threshold in shared memory: only thresholds and counts on the device
         cudaStream_t st = t->st;
-        if (t->bcap_small < count) {
-            if (t->bthr) cudaFreeAsync(t->bthr, st);
-            if (t->bj) cudaFreeAsync(t->bj, st);
-            t->bthr = nullptr;
-            t->bj = nullptr;
-            t->bcap = 0;
-            CK(dalloc(&t->bthr, DECIDE_SMALL_MAX_BATCH, st));
-            CK(dalloc(&t->bj, DECIDE_SMALL_MAX_BATCH, st));
-            t->bcap_small = DECIDE_SMALL_MAX_BATCH;
-        }
+        CK(arena(AR_BTHR, &t->bthr, DECIDE_SMALL_MAX_BATCH, st));
+        CK(arena(AR_BJ, &t->bj, DECIDE_SMALL_MAX_BATCH, st));
         if (!t->pin) CK(cudaMallocHost(&t->pin, 4096));
         double* pthr = static_cast<double*>(t->pin);
         int64_t* pj = reinterpret_cast<int64_t*>(pthr + 64);
@@ -936,24 +957,13 @@ int isoc_decide_batch(isoc_tree* t, const double* thresholds, int32_t count, int
         if (!std::isfinite(thresholds[i])) return fail(ISOC_EINVAL, "threshold must be finite, got %g", thresholds[i]);
     cudaStream_t st = t->st;
     const int64_t n = t->n;
-    if (t->bcap < count) {
-        void* old[] = {t->bom, t->bp, t->bthr, t->bcode, t->bexcl, t->bscratch, t->bj};
-        for (void* q : old)
-            if (q) cudaFreeAsync(q, st);
-        t->bom = t->bp = t->bthr = nullptr;
-        t->bcode = nullptr;
-        t->bexcl = t->bscratch = nullptr;
-        t->bj = nullptr;
-        t->bcap = 0;
-        CK(dalloc(&t->bom, (size_t)count * n, st));
-        CK(dalloc(&t->bp, (size_t)count * n, st));
-        CK(dalloc(&t->bcode, (size_t)count * n, st));
-        CK(dalloc(&t->bexcl, (size_t)count * n, st));
-        CK(dalloc(&t->bscratch, 16 * 1024 + 8, st));
-        CK(dalloc(&t->bthr, 16, st));
-        CK(dalloc(&t->bj, 16, st));
-        t->bcap = count;
-    }
+    CK(arena(AR_BOM, &t->bom, (size_t)count * n, st));
+    CK(arena(AR_BP, &t->bp, (size_t)count * n, st));
+    CK(arena(AR_BCODE, &t->bcode, (size_t)count * n, st));
+    CK(arena(AR_BEXCL, &t->bexcl, (size_t)count * n, st));
+    CK(arena(AR_BSCRATCH, &t->bscratch, 16 * 1024 + 8, st));
+    CK(arena(AR_BTHR, &t->bthr, DECIDE_SMALL_MAX_BATCH, st));
+    CK(arena(AR_BJ, &t->bj, DECIDE_SMALL_MAX_BATCH, st));
     CK(cudaMemcpyAsync(t->bthr, thresholds, (size_t)count * 8, cudaMemcpyHostToDevice, st));
     CK(launch_decide_batch(n, t->levels, t->level_off, t->max_width, t->f_pos, t->om_pos, t->p_pos,
                            t->child_lo, t->child_cnt, t->bthr, count, k, t->bom, t->bp, t->bcode,
@@ -974,14 +984,14 @@ int isoc_witness(isoc_tree* t, int32_t slot, int64_t k, int64_t* labels, int8_t*
     double *sums = nullptr, *miso_d = nullptr;
     void* cwork = nullptr;
     const size_t cbytes = cost_work_bytes(n, k);
-    CK(aalloc(&cut_v, n, st));
-    CK(aalloc(&eta_v, n, st));
-    CK(aalloc(&lab_v, n, st));
-    CK(aalloc(&lab32, n, st));
-    CK(aalloc(&work, 4 * n, st));
-    CK(aalloc(&sums, 3 * k, st));
-    CK(aalloc(&miso_d, 1, st));
-    CK(cudaMallocAsync(&cwork, cbytes, st));
+    CK(arena(AR_CUT, &cut_v, n, st));
+    CK(arena(AR_ETA, &eta_v, n, st));
+    CK(arena(AR_LAB, &lab_v, n, st));
+    CK(arena(AR_LAB32, &lab32, n, st));
+    CK(arena(AR_WORK, &work, 4 * n, st));
+    CK(arena(AR_SUMS, &sums, 3 * k, st));
+    CK(arena(AR_MISO, &miso_d, 1, st));
+    CK(arena(AR_CWORK, reinterpret_cast<unsigned char**>(&cwork), cbytes, st));
     CK(launch_labels(t->code[slot], t->pos_parent, t->bfs, n, t->levels, cut_v, eta_v, lab_v, lab32,
                      work, st));
     // the label / cut / eta read-back (copy engine) overlaps the cost kernels
@@ -1004,10 +1014,7 @@ int isoc_witness(isoc_tree* t, int32_t slot, int64_t k, int64_t* labels, int8_t*
     if (sparsities && t->spars[slot])
         CK(cudaMemcpyAsync(sparsities, t->spars[slot], k * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(miso, miso_d, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamWaitEvent(st, copied, 0));   // buffers stay alive until the copies are done
-    cudaFreeAsync(cut_v, st); cudaFreeAsync(eta_v, st); cudaFreeAsync(lab_v, st);
-    cudaFreeAsync(lab32, st); cudaFreeAsync(work, st); cudaFreeAsync(sums, st);
-    cudaFreeAsync(miso_d, st); cudaFreeAsync(cwork, st);
+    CK(cudaStreamWaitEvent(st, copied, 0));   // the arena buffers are idle once the copies are done
     CK(cudaStreamSynchronize(st));
     return ISOC_OK;
 }
