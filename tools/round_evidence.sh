@@ -5,6 +5,7 @@
 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/ev_gpu_tests.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.log 2>&1
 python bench.py > gpurun_out/ev_bench_c3.jsonl 2> gpurun_out/ev_bench_c3.err
+python bench.py --steps 20 --warmup 3 > gpurun_out/ev_bench_c3_steps20.jsonl 2> gpurun_out/ev_bench_c3_steps20.err
 for c in c1 c2 c4; do python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/ev_bench_$c.jsonl 2> gpurun_out/ev_bench_$c.err; done
 python bench.py --config c5 --steps 5 --warmup 3 > gpurun_out/ev_bench_c5.jsonl 2> gpurun_out/ev_bench_c5.err
 python bench.py --impl reference > gpurun_out/ev_ref_c3.jsonl 2> gpurun_out/ev_ref_c3.err
