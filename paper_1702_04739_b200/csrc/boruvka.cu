@@ -656,21 +656,21 @@ static cudaError_t launch_rescan(const double* X, int64_t n, int d, const int32_
     const size_t cap = (size_t)rescan_capacity(rows, n, sms);
     double *pm1 = nullptr, *pm2 = nullptr;
     int32_t* pj = nullptr;
-    e = cudaMallocAsync((void**)&pm1, cap * 8, st);
+    e = isoc_malloc_async((void**)&pm1, cap * 8, st);
     if (e != cudaSuccess) return e;
-    e = cudaMallocAsync((void**)&pm2, cap * 8, st);
-    if (e != cudaSuccess) { cudaFreeAsync(pm1, st); return e; }
-    e = cudaMallocAsync((void**)&pj, cap * 4, st);
-    if (e != cudaSuccess) { cudaFreeAsync(pm1, st); cudaFreeAsync(pm2, st); return e; }
+    e = isoc_malloc_async((void**)&pm2, cap * 8, st);
+    if (e != cudaSuccess) { isoc_free_async(pm1, st); return e; }
+    e = isoc_malloc_async((void**)&pj, cap * 4, st);
+    if (e != cudaSuccess) { isoc_free_async(pm1, st); isoc_free_async(pm2, st); return e; }
     const int pid = prof_begin(PK_RESCAN, st);
     rescan_tile_kernel<<<sms, 256, RESCAN_SMEM, st>>>(X, n, d, comp, rescan_list, rescan_count, sms, pm1, pm2,
                                                       pj);
     rescan_reduce_kernel<<<sms, 256, 0, st>>>(rescan_list, rescan_count, lo, n, sms, pm1, pm2, pj, cand_d,
                                               cand_j, cand_tie);
     prof_end(pid, st);
-    cudaFreeAsync(pm1, st);
-    cudaFreeAsync(pm2, st);
-    cudaFreeAsync(pj, st);
+    isoc_free_async(pm1, st);
+    isoc_free_async(pm2, st);
+    isoc_free_async(pj, st);
     return cudaGetLastError();
 }
 

@@ -78,13 +78,13 @@ namespace {
 template <typename T>
 cudaError_t dalloc(T** p, size_t count, cudaStream_t st) {
     ensure_pool();
-    return cudaMallocAsync(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), st);
+    return isoc_malloc_async(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), st);
 }
 
 template <typename T>
 cudaError_t aalloc(T** p, size_t count, cudaStream_t st) {
     ensure_pool();
-    return cudaMallocAsync(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), st);
+    return isoc_malloc_async(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), st);
 }
 
 // Per-thread scratch arena for the partition phase (batched sweeps, the
@@ -105,11 +105,11 @@ cudaError_t arena(ArenaSlot slot, T** p, size_t count, cudaStream_t st) {
     const size_t bytes = (count ? count : 1) * sizeof(T);
     Buf& b = bufs[slot];
     if (b.dev != dev || b.bytes < bytes) {
-        if (b.p && b.dev == dev) cudaFreeAsync(b.p, st);
+        if (b.p && b.dev == dev) isoc_free_async(b.p, st);
         b.p = nullptr;
         b.bytes = 0;
         ensure_pool();
-        e = cudaMallocAsync(&b.p, bytes, st);
+        e = isoc_malloc_async(&b.p, bytes, st);
         if (e != cudaSuccess) return e;
         b.bytes = bytes;
         b.dev = dev;
@@ -161,8 +161,8 @@ cudaError_t fold_stacks(const FoldStack* in, int64_t count, FoldStack* out, int3
         FoldStack* t = a; a = b; b = t;
     }
     cudaMemcpyAsync(out, a, sizeof(FoldStack), cudaMemcpyDeviceToDevice, st);
-    cudaFreeAsync(a, st);
-    cudaFreeAsync(b, st);
+    isoc_free_async(a, st);
+    isoc_free_async(b, st);
     return cudaGetLastError();
 }
 }  // namespace
@@ -223,9 +223,9 @@ int isoc_sigma_partial(const double* X, int64_t n, int32_t d, int64_t lo, int64_
         CK(launch_sigma_pass(X, n, d, lo, hi, want_p, row_vals, row_ids, row_cnt, flags, tj, td, tt,
                              want_p ? p_dev : nullptr, st));
         if (!nn_j) {
-            cudaFreeAsync(tj, st);
-            cudaFreeAsync(td, st);
-            cudaFreeAsync(tt, st);
+            isoc_free_async(tj, st);
+            isoc_free_async(td, st);
+            isoc_free_async(tt, st);
         }
     }
     const int64_t b_hi = hi + 1;  // boundaries lo+1 .. hi (boundary n = the final leaf)
@@ -241,9 +241,9 @@ int isoc_sigma_partial(const double* X, int64_t n, int32_t d, int64_t lo, int64_
     }
     int32_t hflags = 0;
     CK(cudaMemcpyAsync(&hflags, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(row_vals, st); cudaFreeAsync(row_ids, st); cudaFreeAsync(row_cnt, st);
-    cudaFreeAsync(sval, st); cudaFreeAsync(sid, st); cudaFreeAsync(sown, st);
-    cudaFreeAsync(groups, st); cudaFreeAsync(flags, st);
+    isoc_free_async(row_vals, st); isoc_free_async(row_ids, st); isoc_free_async(row_cnt, st);
+    isoc_free_async(sval, st); isoc_free_async(sid, st); isoc_free_async(sown, st);
+    isoc_free_async(groups, st); isoc_free_async(flags, st);
     CK(cudaStreamSynchronize(st));
     if (hflags) return fail(ISOC_ECUDA, "pairwise fold stack overflow (flags=%d)", hflags);
     return ISOC_OK;
@@ -275,7 +275,7 @@ int isoc_sigma_sym_range(const double* X, int64_t n, int32_t d, int64_t jlo, int
     CK(launch_sigma_sym_range(X, n, d, jlo, jhi, 1, vals, ids, cnt, flags, m1 ? j1 : nullptr, m1, nullptr, m2, st));
     int32_t hflags = 0;
     CK(cudaMemcpyAsync(&hflags, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(flags, st);
+    isoc_free_async(flags, st);
     CK(cudaStreamSynchronize(st));
     if (hflags) return fail(ISOC_ECUDA, "pairwise fold stack overflow (flags=%d)", hflags);
     return ISOC_OK;
@@ -315,9 +315,9 @@ int isoc_sigma_rank_merge(const double* X, int64_t n, int32_t d, int64_t lo, int
     CK(fold_stacks(groups, ng, reinterpret_cast<FoldStack*>(stack_dev), flags, st));
     int32_t hflags = 0;
     CK(cudaMemcpyAsync(&hflags, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(row_vals, st); cudaFreeAsync(row_ids, st); cudaFreeAsync(row_cnt, st);
-    cudaFreeAsync(sval, st); cudaFreeAsync(sid, st); cudaFreeAsync(sown, st);
-    cudaFreeAsync(groups, st); cudaFreeAsync(flags, st);
+    isoc_free_async(row_vals, st); isoc_free_async(row_ids, st); isoc_free_async(row_cnt, st);
+    isoc_free_async(sval, st); isoc_free_async(sid, st); isoc_free_async(sown, st);
+    isoc_free_async(groups, st); isoc_free_async(flags, st);
     CK(cudaStreamSynchronize(st));
     if (hflags) return fail(ISOC_ECUDA, "pairwise fold stack overflow (flags=%d)", hflags);
     return ISOC_OK;
@@ -334,8 +334,8 @@ int isoc_sigma_finish(const void* stacks_dev, int64_t nseg, double* total_host, 
     CK(fold_stacks(reinterpret_cast<const FoldStack*>(stacks_dev), nseg, out, flags, st));
     FoldStack h;
     CK(cudaMemcpyAsync(&h, out, sizeof(FoldStack), cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(out, st);
-    cudaFreeAsync(flags, st);
+    isoc_free_async(out, st);
+    isoc_free_async(flags, st);
     CK(cudaStreamSynchronize(st));
     if (h.count != 1 || h.id[0] != 1 || h.overflow)
         return fail(ISOC_EINVAL, "fold stacks do not close to one root (count=%d id=%llu)", h.count,
@@ -387,7 +387,7 @@ static void mst_free(isoc_mst* h) {
                     h->counters, h->succ, h->succ2, h->eu, h->ev, h->ed, h->la, h->lb, h->lbo, h->lj,
                     h->blk_flag, h->refresh_rows, h->imgA};
     for (void* p : ptrs)
-        if (p) cudaFreeAsync(p, h->st);
+        if (p) isoc_free_async(p, h->st);
     delete h;
 }
 
@@ -451,7 +451,7 @@ int isoc_mst_create(const double* X, int64_t n, int32_t d, int64_t lo, int64_t h
         uint32_t amb = 0;
         MCK(cudaMemcpyAsync(&amb, am, 4, cudaMemcpyDeviceToHost, h->st));
         MCK(cudaStreamSynchronize(h->st));
-        cudaFreeAsync(am, h->st);
+        isoc_free_async(am, h->st);
         float amax = 0.f;
         memcpy(&amax, &amb, 4);
         int s = 0;  // y * 2^s stays below 2^14 in FP16
@@ -698,7 +698,7 @@ static void tree_free(isoc_tree* t) {
                     t->p_v, t->f_pos, t->om_pos, t->p_pos, t->om_w, t->p_w, t->code[0], t->code[1],
                     t->spars[0], t->spars[1], t->excl, t->scratch, t->j_out};
     for (void* p : ptrs)
-        if (p) cudaFreeAsync(p, t->st);
+        if (p) isoc_free_async(p, t->st);
     if (t->side) {
         cudaStreamSynchronize(t->side);
         cudaStreamDestroy(t->side);
@@ -885,7 +885,7 @@ int isoc_tree_set_weights(isoc_tree* t, const double* omega, const double* p, do
         CK(aalloc(&key, 3, st));
         CK(launch_extrema(t->flow_v, t->root, t->omega_v, t->p_v, n, out6, tmp, key, st));
         CK(cudaMemcpyAsync(extrema, out6, 6 * 8, cudaMemcpyDeviceToHost, st));
-        cudaFreeAsync(out6, st); cudaFreeAsync(tmp, st); cudaFreeAsync(key, st);
+        isoc_free_async(out6, st); isoc_free_async(tmp, st); isoc_free_async(key, st);
         CK(cudaStreamSynchronize(st));
     }
     return ISOC_OK;
@@ -898,7 +898,7 @@ int isoc_decide(isoc_tree* t, double N, int64_t k, int32_t slot, int64_t* j_host
     if (slot < 0 || slot > 1) return fail(ISOC_EINVAL, "slot must be 0 or 1");
     cudaStream_t st = t->st;
     if (t->spars_cap[slot] < k) {
-        if (t->spars[slot]) cudaFreeAsync(t->spars[slot], t->st);
+        if (t->spars[slot]) isoc_free_async(t->spars[slot], t->st);
         t->spars[slot] = nullptr;
         CK(dalloc(&t->spars[slot], k, t->st));
         t->spars_cap[slot] = k;
@@ -1036,11 +1036,11 @@ int isoc_tree_cost(isoc_tree* t, const int64_t* labels, int64_t k, double* miso)
     CK(aalloc(&lab32, n, st));
     CK(aalloc(&sums, 3 * k, st));
     CK(aalloc(&miso_d, 1, st));
-    CK(cudaMallocAsync(&cwork, cbytes, st));
+    CK(isoc_malloc_async(&cwork, cbytes, st));
     labels_to_i32_kernel<<<blocks(n, 256), 256, 0, st>>>(labels, n, lab32);
     CK(launch_cost(lab32, t->parent_v, t->flow_v, t->omega_v, t->p_v, n, k, cwork, cbytes, sums, miso_d, st));
     CK(cudaMemcpyAsync(miso, miso_d, 8, cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(lab32, st); cudaFreeAsync(sums, st); cudaFreeAsync(miso_d, st); cudaFreeAsync(cwork, st);
+    isoc_free_async(lab32, st); isoc_free_async(sums, st); isoc_free_async(miso_d, st); isoc_free_async(cwork, st);
     CK(cudaStreamSynchronize(st));
     return ISOC_OK;
 }

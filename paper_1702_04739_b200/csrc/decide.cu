@@ -750,10 +750,10 @@ cudaError_t launch_labels(const int8_t* code, const int32_t* pos_parent, const i
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, cut_i, scan, (int)n, st);
     void* tmp = nullptr;
-    cudaError_t e = cudaMallocAsync(&tmp, tb, st);
+    cudaError_t e = isoc_malloc_async(&tmp, tb, st);
     if (e != cudaSuccess) return e;
     cub::DeviceScan::ExclusiveSum(tmp, tb, cut_i, scan, (int)n, st);
-    cudaFreeAsync(tmp, st);
+    isoc_free_async(tmp, st);
     labels_kernel<<<nb(n, 256), 256, 0, st>>>(rep, code, bfs, scan, n, eta, labels, lab32);
     note_launch(passes + 3);
     return cudaGetLastError();
@@ -1003,11 +1003,11 @@ cudaError_t launch_cost(const int32_t* lab32, const int32_t* parent_v, const dou
     cub::DeviceRadixSort::SortPairs(nullptr, tb2, bkeys, bkeys_s, bvals, bvals_s, (int)(2 * n), 0, bits,
                                     st);
     void* tmp = nullptr;
-    cudaError_t e = cudaMallocAsync(&tmp, tb1 > tb2 ? tb1 : tb2, st);
+    cudaError_t e = isoc_malloc_async(&tmp, tb1 > tb2 ? tb1 : tb2, st);
     if (e != cudaSuccess) return e;
     cub::DeviceRadixSort::SortPairs(tmp, tb1, mkeys, mkeys_s, mvals, mvals_s, (int)n, 0, bits, st);
     cub::DeviceRadixSort::SortPairs(tmp, tb2, bkeys, bkeys_s, bvals, bvals_s, (int)(2 * n), 0, bits, st);
-    cudaFreeAsync(tmp, st);
+    isoc_free_async(tmp, st);
     segment_bounds_kernel<<<nb(k + 1, 128), 128, 0, st>>>(mkeys_s, n, k, mseg);
     segment_bounds_kernel<<<nb(k + 1, 128), 128, 0, st>>>(bkeys_s, 2 * n, k, bseg);
     slot_offsets_kernel<<<1, 1, 0, st>>>(bseg, mseg, k, blk_off);

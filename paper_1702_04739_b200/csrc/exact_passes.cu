@@ -628,7 +628,7 @@ static cudaError_t make_xt(const double* X, int64_t n, int d, double** XT, int64
                            cudaStream_t st) {
     *np = (n + XN - 1) / XN * XN + XN;
     *dpad = (d + XK - 1) / XK * XK;
-    cudaError_t e = cudaMallocAsync((void**)XT, (size_t)(*np) * (*dpad) * sizeof(double), st);
+    cudaError_t e = isoc_malloc_async((void**)XT, (size_t)(*np) * (*dpad) * sizeof(double), st);
     if (e != cudaSuccess) return e;
     return launch_transpose_pad(X, n, d, *np, *dpad, *XT, st);
 }
@@ -653,7 +653,7 @@ cudaError_t launch_sigma_pass(const double* X, int64_t n, int d, int64_t lo, int
                                               row_cnt, flags, nn_j, nn_d, nn_tie, pfold);
     prof_end(pid, st);
     note_launch();
-    cudaFreeAsync(XT, st);
+    isoc_free_async(XT, st);
     return cudaGetLastError();
 }
 
@@ -708,7 +708,7 @@ cudaError_t launch_omega_pass(const double* X, int64_t n, int d, int64_t lo, int
                                                nn_j, nn_d, nn_tie);
     prof_end(pid, st);
     note_launch();
-    cudaFreeAsync(XT, st);
+    isoc_free_async(XT, st);
     return cudaGetLastError();
 }
 

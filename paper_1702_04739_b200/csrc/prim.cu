@@ -151,7 +151,7 @@ static int prim_launch(bool dense, const double* X, int64_t n, int32_t d, int64_
     if ((int64_t)G * PRIM_THREADS > n) G = (int)((n + PRIM_THREADS - 1) / PRIM_THREADS);
     char* scratch = nullptr;
     const size_t bytes = (size_t)n * (8 + 4 + 1) + 2 * need * 16 + 64 + 16;
-    cudaError_t e = cudaMallocAsync((void**)&scratch, bytes, st);
+    cudaError_t e = isoc::isoc_malloc_async((void**)&scratch, bytes, st);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return isoc::set_error(e == cudaErrorMemoryAllocation ? ISOC_ENOMEM : ISOC_ECUDA,
@@ -167,7 +167,7 @@ static int prim_launch(bool dense, const double* X, int64_t n, int32_t d, int64_
     int dd = d;
     void* args[] = {(void*)&X, &n, &dd, &root, &key, &from, &done, &pv, &pi, &u, &v, &w, &bar};
     e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(PRIM_THREADS), args, 0, st);
-    cudaFreeAsync(scratch, st);
+    isoc::isoc_free_async(scratch, st);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return isoc::set_error(ISOC_ECUDA, "prim_kernel launch: %s", cudaGetErrorString(e));

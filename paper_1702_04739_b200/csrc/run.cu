@@ -35,7 +35,7 @@ struct DevBuf {
     void* p = nullptr;
     cudaStream_t st = nullptr;
     ~DevBuf() {
-        if (p) cudaFreeAsync(p, st);
+        if (p) isoc::isoc_free_async(p, st);
     }
     template <typename T>
     T* get() const { return static_cast<T*>(p); }
@@ -59,7 +59,7 @@ inline double now_ms() {
 
 int alloc(DevBuf& b, size_t bytes, cudaStream_t st) {
     b.st = st;
-    const cudaError_t e = cudaMallocAsync(&b.p, bytes ? bytes : 1, st);
+    const cudaError_t e = isoc::isoc_malloc_async(&b.p, bytes ? bytes : 1, st);
     if (e != cudaSuccess)
         return isoc::set_error(e == cudaErrorMemoryAllocation ? ISOC_ENOMEM : ISOC_ECUDA, "%s",
                                cudaGetErrorString(e));

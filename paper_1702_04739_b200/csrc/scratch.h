@@ -5,6 +5,9 @@
 
 namespace isoc {
 
+cudaError_t isoc_malloc_async(void** p, size_t bytes, cudaStream_t st);   // alloc.cu
+cudaError_t isoc_free_async(void* p, cudaStream_t st);
+
 struct Scratch {
     cudaStream_t st;
     void* ptrs[16];
@@ -15,12 +18,12 @@ struct Scratch {
     template <typename T>
     cudaError_t alloc(T** p, size_t elems) {
         if (count >= 16) return cudaErrorMemoryAllocation;
-        cudaError_t e = cudaMallocAsync((void**)p, (elems ? elems : 1) * sizeof(T), st);
+        cudaError_t e = isoc_malloc_async((void**)p, (elems ? elems : 1) * sizeof(T), st);
         if (e == cudaSuccess) ptrs[count++] = *p;
         return e;
     }
     ~Scratch() {
-        for (int i = 0; i < count; ++i) cudaFreeAsync(ptrs[i], st);
+        for (int i = 0; i < count; ++i) isoc_free_async(ptrs[i], st);
     }
 };
 

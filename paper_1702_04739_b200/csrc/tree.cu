@@ -362,10 +362,10 @@ cudaError_t launch_build_adjacency(const int32_t* eu, const int32_t* ev, const d
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, deg, off, (int)(n + 1), st);
     void* tmp = nullptr;
-    cudaError_t e = cudaMallocAsync(&tmp, tb, st);
+    cudaError_t e = isoc_malloc_async(&tmp, tb, st);
     if (e != cudaSuccess) return e;
     cub::DeviceScan::ExclusiveSum(tmp, tb, deg, off, (int)(n + 1), st);
-    cudaFreeAsync(tmp, st);
+    isoc_free_async(tmp, st);
     cudaMemcpyAsync(deg, off, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
     if (m > 0) fill_adj_kernel<<<nblk(m, 256), 256, 0, st>>>(eu, ev, ed, m, deg, adj, adjd);
     sort_adj_kernel<<<nblk(n, 256), 256, 0, st>>>(off, n, adj, adjd);
@@ -381,11 +381,11 @@ cudaError_t launch_children_from_parent(const int64_t* parent, const int64_t* ch
     int32_t *vals = nullptr, *pkeys = nullptr, *deg = nullptr;
     cudaError_t e;
 #define ACK(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
-    ACK(cudaMallocAsync((void**)&keys, (size_t)n * 8, st));
-    ACK(cudaMallocAsync((void**)&skeys, (size_t)n * 8, st));
-    ACK(cudaMallocAsync((void**)&vals, (size_t)n * 4, st));
-    ACK(cudaMallocAsync((void**)&pkeys, (size_t)n * 4, st));
-    ACK(cudaMallocAsync((void**)&deg, (size_t)(n + 1) * 4, st));
+    ACK(isoc_malloc_async((void**)&keys, (size_t)n * 8, st));
+    ACK(isoc_malloc_async((void**)&skeys, (size_t)n * 8, st));
+    ACK(isoc_malloc_async((void**)&vals, (size_t)n * 4, st));
+    ACK(isoc_malloc_async((void**)&pkeys, (size_t)n * 4, st));
+    ACK(isoc_malloc_async((void**)&deg, (size_t)(n + 1) * 4, st));
     cudaMemsetAsync(nroots, 0, sizeof(int32_t), st);
     parent_check_kernel<<<nblk(n, 256), 256, 0, st>>>(parent, child_id, n, root, keys, vals, pkeys,
                                                        flags, nroots, found_root);
@@ -394,20 +394,20 @@ cudaError_t launch_children_from_parent(const int64_t* parent, const int64_t* ch
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, skeys, vals, adj, (int)n, 0, bits, st);
     void* tmp = nullptr;
-    ACK(cudaMallocAsync(&tmp, tb, st));
+    ACK(isoc_malloc_async(&tmp, tb, st));
     cub::DeviceRadixSort::SortPairs(tmp, tb, keys, skeys, vals, adj, (int)n, 0, bits, st);
-    cudaFreeAsync(tmp, st);
+    isoc_free_async(tmp, st);
     cudaMemsetAsync(deg, 0, (size_t)(n + 1) * sizeof(int32_t), st);
     count_children_kernel<<<nblk(n, 256), 256, 0, st>>>(pkeys, n, deg);
     tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, deg, off, (int)(n + 1), st);
-    ACK(cudaMallocAsync(&tmp, tb, st));
+    ACK(isoc_malloc_async(&tmp, tb, st));
     cub::DeviceScan::ExclusiveSum(tmp, tb, deg, off, (int)(n + 1), st);
-    cudaFreeAsync(tmp, st);
+    isoc_free_async(tmp, st);
     child_ids_kernel<<<nblk(n, 256), 256, 0, st>>>(skeys, adj, off, n, child_id_v);
     note_launch(3);
-    cudaFreeAsync(keys, st); cudaFreeAsync(skeys, st); cudaFreeAsync(vals, st);
-    cudaFreeAsync(pkeys, st); cudaFreeAsync(deg, st);
+    isoc_free_async(keys, st); isoc_free_async(skeys, st); isoc_free_async(vals, st);
+    isoc_free_async(pkeys, st); isoc_free_async(deg, st);
 #undef ACK
     return cudaGetLastError();
 }
