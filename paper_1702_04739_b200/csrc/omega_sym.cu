@@ -246,14 +246,17 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                 compv = g < n ? comp[g] : (ttid < TBM ? -1 : -2);
             }
         }
+        // chunk it's copies (the only group in flight) land; after the team
+        // barrier every thread has also left chunk it-1, so its buffer takes
+        // chunk it+1's copies while chunk it computes (one barrier per chunk)
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        team_sync(team);
         if (it + 1 < total) {
             const int k1 = (kc + 1 == nk) ? 0 : kc + 1;
             const int t1 = (kc + 1 == nk) ? tile + 1 : tile;
             sym_load(ts.st[(it + 1) & 1], XT, np, R0 + (t1 / TJ) * TBM, C0 + (t1 % TJ) * TBN, k1, ttid);
         }
         asm volatile("cp.async.commit_group;\n" ::);
-        asm volatile("cp.async.wait_group 1;\n" ::);
-        team_sync(team);
         // the tile's component ids go to shared memory only now: every thread
         // of the team has left the previous tile's epilogue (which reads them;
         // a diagonal tile's epilogue ends without a team barrier)
@@ -280,7 +283,6 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                     for (int j = 0; j < 8; ++j) acc[i][j] = exact_sq_step(acc[i][j], a[i], bv[j]);
             }
         }
-        team_sync(team);
         if (++kc != nk) continue;
         kc = 0;
         ++tile;
