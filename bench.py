@@ -349,6 +349,16 @@ def reference_arm(args):
 KIND_NAMES = ["sigma_pass", "omega_pass", "boruvka_filter", "decide", "rescan", "bfs", "cost"]
 
 
+def pinned_copy(a):
+    """The e2e contract's inputs live in page-locked host memory: a pinned
+    numpy array with a's contents (the library copies it straight to HBM)."""
+    import torch
+    a = np.ascontiguousarray(a)
+    out = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True).numpy()
+    np.copyto(out, a)
+    return out
+
+
 def tree_phase_bench(args):
     """C5: tree phase only on a 50M-vertex random recursive tree, k = 100
     (tree_from_parent_list + extrema + par_solve_miso), vertices/s."""
@@ -357,7 +367,7 @@ def tree_phase_bench(args):
 
     n = args.n or 50_000_000
     k = args.k or 100
-    parent, flows, omega, p = synthetic_tree(n, 0)
+    parent, flows, omega, p = (pinned_copy(a) for a in synthetic_tree(n, 0))
     w = pkg.NodeWeights(omega=omega, p=p, sigma=1.0, alpha=0.0)
 
     def step():
@@ -518,7 +528,7 @@ def main():
 
     n, d, k = workload(args)
     X, _ = pkg_generate_random(n, d, k, 0)
-    X = np.ascontiguousarray(X)
+    X = pinned_copy(X)
     Xdev = torch.from_numpy(X).pin_memory().cuda()
     torch.cuda.synchronize()
 
