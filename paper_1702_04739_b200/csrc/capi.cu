@@ -118,6 +118,39 @@ cudaError_t arena(ArenaSlot slot, T** p, size_t count, cudaStream_t st) {
     return cudaSuccess;
 }
 
+// Per-thread page-locked staging (4 KB) for the small read-backs of the MST
+// rounds and the sweeps (each use copies, synchronizes and reads within one
+// call), and the witness's side stream: created once per thread and device,
+// not per handle -- cudaMallocHost / cudaFreeHost / stream creation on every
+// pipeline run were part of the same random host stalls as the allocations.
+static void* host_stage() {
+    struct Pin { void* p = nullptr; };
+    static thread_local Pin pin;
+    if (!pin.p && cudaMallocHost(&pin.p, 4096) != cudaSuccess) pin.p = nullptr;
+    return pin.p;
+}
+
+struct SideStream {
+    int dev = -1;
+    cudaStream_t s = nullptr;
+    cudaEvent_t ready = nullptr, copied = nullptr;
+};
+static cudaError_t side_stream(SideStream** out) {
+    static thread_local SideStream side;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (side.dev != dev) {   // first use on this device (a previous device's stream is left to the context)
+        e = cudaStreamCreateWithFlags(&side.s, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&side.ready, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&side.copied, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+        side.dev = dev;
+    }
+    *out = &side;
+    return cudaSuccess;
+}
+
 __global__ void scale_kernel(double* v, int64_t m, double a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) v[i] = __dmul_rn(a, v[i]);
@@ -381,7 +414,6 @@ struct isoc_mst {
 
 static void mst_free(isoc_mst* h) {
     if (!h) return;
-    if (h->pin) cudaFreeHost(h->pin);
     void* ptrs[] = {h->img, h->Y, h->ny, h->rad, h->centre, h->rmax, h->comp, h->a1, h->a2, h->j1,
                     h->compB, h->cand_d, h->cand_j, h->cand_state, h->cand_tie, h->rescan_list,
                     h->counters, h->succ, h->succ2, h->eu, h->ev, h->ed, h->la, h->lb, h->lbo, h->lj,
@@ -514,7 +546,8 @@ int isoc_mst_round_local(isoc_mst* h, int use_nn, const int32_t* nn_j, const dou
                 CK(launch_list_refresh(h->a1, h->lbo, h->rad, h->comp, h->n, h->lo, h->hi, h->rmax, h->cd,
                                        h->cabs, h->compB, h->blk_flag, h->nblk, h->counters + 5,
                                        h->refresh_rows, st));
-                if (!h->pin) CK(cudaMallocHost((void**)&h->pin, 64));
+                h->pin = static_cast<int32_t*>(host_stage());
+                if (!h->pin) return fail(ISOC_ECUDA, "page-locked staging unavailable");
                 CK(cudaMemcpyAsync(h->pin + 8, h->counters + 5, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
                 const int32_t nf[2] = {h->pin[8], h->pin[9]};   // flagged blocks, rows
@@ -558,7 +591,8 @@ int isoc_mst_round_finish(isoc_mst* h, const uint64_t* comp_min, const uint64_t*
                         ce, h->counters + 1, st));
     CK(launch_hook_contract(h->comp, h->n, cm, ce, h->succ, h->succ2, h->eu, h->ev, h->ed,
                             h->counters + 2, h->counters + 3, h->counters + 4, st));
-    if (!h->pin) CK(cudaMallocHost((void**)&h->pin, 64));
+    h->pin = static_cast<int32_t*>(host_stage());
+    if (!h->pin) return fail(ISOC_ECUDA, "page-locked staging unavailable");
     CK(cudaMemcpyAsync(h->pin, h->counters, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     int32_t c[8];
@@ -685,13 +719,9 @@ struct isoc_tree {
     int8_t* bcode;
     int32_t *bexcl, *bscratch;
     int64_t* bj;
-    // witness read-back overlap (isoc_witness), created on first use
-    cudaStream_t side;
-    cudaEvent_t ev_ready, ev_copied;
 };
 
 static void tree_free(isoc_tree* t) {
-    if (t && t->pin) cudaFreeHost(t->pin);
     if (!t) return;
     void* ptrs[] = {t->bfs, t->pos_of, t->parent_v, t->depth_v, t->child_id_v, t->pos_parent,
                     t->child_lo, t->child_cnt, t->parent_d, t->flow_v, t->level_off, t->omega_v,
@@ -699,12 +729,6 @@ static void tree_free(isoc_tree* t) {
                     t->spars[0], t->spars[1], t->excl, t->scratch, t->j_out};
     for (void* p : ptrs)
         if (p) isoc_free_async(p, t->st);
-    if (t->side) {
-        cudaStreamSynchronize(t->side);
-        cudaStreamDestroy(t->side);
-        cudaEventDestroy(t->ev_ready);
-        cudaEventDestroy(t->ev_copied);
-    }
     delete t;
 }
 
@@ -903,7 +927,8 @@ int isoc_decide(isoc_tree* t, double N, int64_t k, int32_t slot, int64_t* j_host
         CK(dalloc(&t->spars[slot], k, t->st));
         t->spars_cap[slot] = k;
     }
-    if (!t->pin) CK(cudaMallocHost(&t->pin, 4096));
+    t->pin = host_stage();
+    if (!t->pin) return fail(ISOC_ECUDA, "page-locked staging unavailable");
     CK(launch_decide(t->n, t->levels, t->level_off, t->max_width, t->f_pos, t->om_pos, t->p_pos,
                      t->child_lo, t->child_cnt, N, k, t->om_w, t->p_w, t->code[slot], t->excl,
                      t->spars[slot], t->scratch, t->j_out, st));
@@ -940,7 +965,8 @@ int isoc_decide_batch(isoc_tree* t, const double* thresholds, int32_t count, int
         cudaStream_t st = t->st;
         CK(arena(AR_BTHR, &t->bthr, DECIDE_SMALL_MAX_BATCH, st));
         CK(arena(AR_BJ, &t->bj, DECIDE_SMALL_MAX_BATCH, st));
-        if (!t->pin) CK(cudaMallocHost(&t->pin, 4096));
+        t->pin = host_stage();
+        if (!t->pin) return fail(ISOC_ECUDA, "page-locked staging unavailable");
         double* pthr = static_cast<double*>(t->pin);
         int64_t* pj = reinterpret_cast<int64_t*>(pthr + 64);
         memcpy(pthr, thresholds, (size_t)count * 8);
@@ -996,13 +1022,10 @@ int isoc_witness(isoc_tree* t, int32_t slot, int64_t k, int64_t* labels, int8_t*
                      work, st));
     // the label / cut / eta read-back (copy engine) overlaps the cost kernels
     // (SMs): a side stream waits for the labels, the main stream goes on
-    if (!t->side) {
-        CK(cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&t->ev_ready, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&t->ev_copied, cudaEventDisableTiming));
-    }
-    cudaStream_t side = t->side;
-    cudaEvent_t ready = t->ev_ready, copied = t->ev_copied;
+    SideStream* ss = nullptr;
+    CK(side_stream(&ss));
+    cudaStream_t side = ss->s;
+    cudaEvent_t ready = ss->ready, copied = ss->copied;
     CK(cudaEventRecord(ready, st));
     CK(cudaStreamWaitEvent(side, ready, 0));
     if (labels) CK(cudaMemcpyAsync(labels, lab_v, n * 8, cudaMemcpyDeviceToHost, side));

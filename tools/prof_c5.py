@@ -12,7 +12,7 @@ import bench  # noqa: E402
 import paper_1702_04739_b200 as pkg  # noqa: E402
 
 n, k = 50_000_000, 100
-parent, flows, omega, p = bench.synthetic_tree(n, 0)
+parent, flows, omega, p = (bench.pinned_copy(a) for a in bench.synthetic_tree(n, 0))
 w = pkg.NodeWeights(omega=omega, p=p, sigma=1.0, alpha=0.0)
 
 
