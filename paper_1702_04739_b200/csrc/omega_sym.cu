@@ -50,6 +50,8 @@ struct TeamSmem {
     int32_t xcj[8][TBN];
     double rmin[TBM];
     int32_t rminj[TBM];
+    uint64_t trm[4][TEAM];     // per-thread running row minima over the column tiles
+    int32_t trj[4][TEAM];
     double cmin[HALF];
     int32_t cminj[HALF];
     int32_t comp_r[TBM];       // component ids of the tile's rows / columns
@@ -341,20 +343,26 @@ omega_sym_kernel(const double* __restrict__ XT, int64_t np, int dpad, int64_t n,
                         if (ok && bv < m) { m = bv; mj = (int32_t)(gcb + LCOL(j)); }
                         else if (ok && bv == m) mj |= TIEBIT;
                     }
+                    // the thread's running minimum over the team's column tiles;
+                    // one merge across the row's 8 lanes after the last tile
+                    // (the merge is associative: min value, min column, tie
+                    // flag iff the minimum occurs twice)
+                    if (tj > 0) tie_merge_bits(m, mj, ts.trm[i][ttid], ts.trj[i][ttid]);
+                    if (tj + 1 < TJ) {
+                        ts.trm[i][ttid] = m;
+                        ts.trj[i][ttid] = mj;
+                    } else {
 #pragma unroll
-                    for (int off = 1; off < 8; off <<= 1) {
-                        const uint64_t om = (uint64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off);
-                        const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
-                        tie_merge_bits(m, mj, om, oj);
-                    }
-                    if (cl == 0) {
-                        const int r = rg * 4 + i;
-                        const double md = __longlong_as_double((long long)m);
-                        double pm = tj == 0 ? INFINITY : ts.rmin[r];
-                        int32_t pj = tj == 0 ? INT32_MAX : ts.rminj[r];
-                        tie_merge(pm, pj, md, mj);
-                        ts.rmin[r] = pm;
-                        ts.rminj[r] = pj;
+                        for (int off = 1; off < 8; off <<= 1) {
+                            const uint64_t om = (uint64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off);
+                            const int32_t oj = __shfl_xor_sync(0xffffffffu, mj, off);
+                            tie_merge_bits(m, mj, om, oj);
+                        }
+                        if (cl == 0) {
+                            const int r = rg * 4 + i;
+                            ts.rmin[r] = __longlong_as_double((long long)m);
+                            ts.rminj[r] = mj;
+                        }
                     }
                 }
                 // column minima over the thread's rows (ascending), then the warp
