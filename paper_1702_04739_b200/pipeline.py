@@ -401,6 +401,19 @@ def _speculation_depth(dt: DeviceTree) -> int:
     return 4 if dt.n <= 64 * 1024 * max(1, levels) and width <= 262144 else 1
 
 
+_HEAP_KIDS: dict = {}
+
+
+def _heap_kids(depth: int) -> list:
+    """kids of the complete depth-`depth` tree in heap order (read-only, cached)."""
+    kids = _HEAP_KIDS.get(depth)
+    if kids is None:
+        m = (1 << depth) - 1
+        kids = [[2 * i + 1, 2 * i + 2] if 2 * i + 1 < m else [-1, -1] for i in range(m)]
+        _HEAP_KIDS[depth] = kids
+    return kids
+
+
 def _threshold_tree(a0: float, b0: float, depth: int):
     """The midpoints the next `depth` bisection steps can visit from the
     bracket (a0, b0): node = (a + b) / 2 of its interval, children the
@@ -408,6 +421,24 @@ def _threshold_tree(a0: float, b0: float, depth: int):
     reference's stop test b - a <= 1e-15 * max(1, b) (isoperim.py:263-266)
     does not exist, nor do its descendants.  Built in level order.  Returns
     (thresholds, kids[node] = [left, right] or -1, root or -1)."""
+    if depth >= 1 and (b0 - a0) / float(1 << (depth - 1)) > 4.0 * BRACKET_EPS * max(1.0, b0):
+        # no interval of the tree can pass the stop test (each is at least
+        # (b0 - a0) / 2^(depth-1) wide up to rounding, and b <= b0): the
+        # complete tree in heap order, which is the level order below
+        m = (1 << depth) - 1
+        lo = [0.0] * m
+        hi = [0.0] * m
+        thr = [0.0] * m
+        lo[0], hi[0] = a0, b0
+        half = m >> 1
+        for i in range(m):
+            a, b = lo[i], hi[i]
+            mid = (a + b) / 2.0
+            thr[i] = mid
+            if i < half:
+                c = 2 * i + 1
+                lo[c], hi[c], lo[c + 1], hi[c + 1] = a, mid, mid, b
+        return thr, _heap_kids(depth), 0
     thr: list = []
     kids: list = []
     root = -1
