@@ -825,8 +825,7 @@ cudaError_t launch_boruvka_filter(const float* Y, const float* ny, const int32_t
                                   float* a2, cudaStream_t st) {
     if (hi <= lo) return cudaSuccess;
     const size_t smem = sizeof(FilterSmem);
-    cudaError_t e = cudaFuncSetAttribute(boruvka_filter_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_max_dyn_smem((const void*)boruvka_filter_kernel, (size_t)((int)smem));
     if (e != cudaSuccess) return e;
     const int pid = prof_begin(PK_FILTER, st);
     boruvka_filter_kernel<<<blocks_for(hi - lo, FM), FT, smem, st>>>(Y, ny, comp, n, npad, dp, lo, hi,

@@ -118,6 +118,18 @@ cudaError_t arena(ArenaSlot slot, T** p, size_t count, cudaStream_t st) {
     return cudaSuccess;
 }
 
+static size_t device_total_memory() {
+    static size_t cache[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cache[dev] == 0) {
+        cudaDeviceProp prop;
+        cache[dev] = cudaGetDeviceProperties(&prop, dev) == cudaSuccess ? prop.totalGlobalMem : ((size_t)80 << 30);
+    }
+    return cache[dev];
+}
+
 // Per-thread page-locked staging (4 KB) for the small read-backs of the MST
 // rounds and the sweeps (each use copies, synchronizes and reads within one
 // call), and the witness's side stream: created once per thread and device,
@@ -654,15 +666,20 @@ int isoc_omega_mst(const double* X, int64_t n, int32_t d, int64_t lo, int64_t hi
     const int mode = passes_mode();
     const bool sym_wide = mode == 1 || (mode == 0 && nbs * (nbs + 1) / 2 >= device_sm_count());
     bool sym = lo == 0 && hi == n && sym_wide;
-    if (sym) {   // (cudaMemGetInfo costs ~1 ms: only when the symmetric pass is a candidate)
-        size_t free_b = 0, total_b = 0;
-        cudaMemGetInfo(&free_b, &total_b);
+    if (sym) {   // against the device's capacity (queried once: no driver query per call)
         const double ps_bytes = (double)nbs * (double)n * (comp ? 20.0 : 8.0);
-        sym = ps_bytes < 0.6 * (double)free_b;
+        sym = ps_bytes < 0.35 * (double)device_total_memory();
     }
     if (sym) {
-        CK(launch_omega_sym(X, n, d, sigma, comp, omega, nn_j, nn_d, nn_tie, (cudaStream_t)stream));
-    } else {
+        const cudaError_t e = launch_omega_sym(X, n, d, sigma, comp, omega, nn_j, nn_d, nn_tie, (cudaStream_t)stream);
+        if (e == cudaErrorMemoryAllocation) {   // the slot buffers did not fit after all: row pass
+            cudaGetLastError();
+            sym = false;
+        } else {
+            CK(e);
+        }
+    }
+    if (!sym) {
         CK(launch_omega_pass(X, n, d, lo, hi, sigma, comp, omega, nn_j, nn_d, nn_tie,
                              (cudaStream_t)stream));
     }

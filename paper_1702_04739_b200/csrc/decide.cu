@@ -593,13 +593,27 @@ bool decide_small_fits(int64_t n, int64_t levels, size_t* smem) {
     return *smem <= (size_t)optin;
 }
 
+// Resident 512-thread CTAs per SM of the cooperative sweep kernels, queried
+// once per device (slot 0: decide_kernel, 1: decide_batch_kernel).
+static int resident_per_sm(const void* kern, int slot) {
+    static int cache[64][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cache[dev][slot] == 0) {
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, 0);
+        cache[dev][slot] = per_sm > 0 ? per_sm : 1;
+    }
+    return cache[dev][slot];
+}
+
 static cudaError_t launch_decide_small(int64_t n, int64_t levels, const int64_t* level_off, const double* f_pos,
                                        const double* om0, const double* p0, const int32_t* child_lo,
                                        const int32_t* child_cnt, const double* thr, int K, int64_t k,
                                        int8_t* code, double* spars, int64_t* j_out, size_t smem,
                                        cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(decide_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = ensure_max_dyn_smem((const void*)decide_small_kernel, (size_t)((int)smem));
     if (e != cudaSuccess) return e;
     DecideSmallArgs A;
     A.n = n; A.levels = levels; A.level_off = level_off; A.f_pos = f_pos; A.om0 = om0; A.p0 = p0;
@@ -623,11 +637,7 @@ cudaError_t launch_decide_batch(int64_t n, int64_t levels, const int64_t* level_
     if (decide_small_fits(n, levels, &smem))
         return launch_decide_small(n, levels, level_off, f_pos, om0, p0, child_lo, child_cnt, thr, K, k,
                                    nullptr, nullptr, j_out, smem, st);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decide_batch_kernel, 512, 0);
-    const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    const int64_t cap = (int64_t)device_sm_count() * resident_per_sm((const void*)decide_batch_kernel, 1);
     int64_t gi = (max_width + 8191) / 8192;
     if (gi < 1) gi = 1;
     if (gi * K > cap) gi = cap / K > 0 ? cap / K : 1;
@@ -648,12 +658,8 @@ cudaError_t launch_decide_batch(int64_t n, int64_t levels, const int64_t* level_
 }
 
 int decide_grid_size(int64_t max_width) {
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decide_kernel, 512, 0);
     int64_t want = (max_width + 8191) / 8192;
-    int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    int64_t cap = (int64_t)device_sm_count() * resident_per_sm((const void*)decide_kernel, 0);
     if (cap > DK_MAXG) cap = DK_MAXG;
     if (want < 1) want = 1;
     return (int)(want < cap ? want : cap);

@@ -645,7 +645,7 @@ cudaError_t launch_sigma_pass(const double* X, int64_t n, int d, int64_t lo, int
     cudaError_t e = make_xt(X, n, d, &XT, &np, &dpad, st);
     if (e != cudaSuccess) return e;
     const size_t smem = sizeof(SigmaSmem);
-    e = cudaFuncSetAttribute(sigma_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = ensure_max_dyn_smem((const void*)sigma_pass_kernel, (size_t)((int)smem));
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((rows + XM - 1) / XM);
     const int pid = prof_begin(PK_SIGMA, st);
@@ -700,7 +700,7 @@ cudaError_t launch_omega_pass(const double* X, int64_t n, int d, int64_t lo, int
     cudaError_t e = make_xt(X, n, d, &XT, &np, &dpad, st);
     if (e != cudaSuccess) return e;
     const size_t smem = sizeof(OmegaSmem);
-    e = cudaFuncSetAttribute(omega_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = ensure_max_dyn_smem((const void*)omega_pass_kernel, (size_t)((int)smem));
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((rows + XM - 1) / XM);
     const int pid = prof_begin(PK_OMEGA, st);

@@ -535,13 +535,13 @@ cudaError_t launch_filter_tc(const uint8_t* img, const float* ny, const int32_t*
     cudaError_t e;
     if (KA == 1) {
         const size_t smem = sizeof(TcSmemT<false>) + 1024;
-        e = cudaFuncSetAttribute(filter_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = ensure_max_dyn_smem((const void*)filter_tc_kernel<false>, (size_t)((int)smem));
         if (e != cudaSuccess) return e;
         filter_tc_kernel<false><<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, la, lj, lb,
                                                                  imgA, rows_map, nmap, 1);
     } else {
         const size_t smem = sizeof(TcSmemT<true>) + 1024;
-        e = cudaFuncSetAttribute(filter_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = ensure_max_dyn_smem((const void*)filter_tc_kernel<true>, (size_t)((int)smem));
         if (e != cudaSuccess) return e;
         filter_tc_kernel<true><<<grid, TC_THREADS, smem, st>>>(img, ny, comp, n, lo, hi, kscale, la, lj, lb,
                                                                 imgA, rows_map, nmap, KA);

@@ -647,7 +647,7 @@ static cudaError_t omega_sym_tiles(const double* X, int64_t n, int d, double sig
     e = launch_transpose_pad(X, n, d, np, dpad, XT, st);
     if (e != cudaSuccess) return e;
     const size_t smem = sizeof(SymSmem);
-    e = cudaFuncSetAttribute(omega_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = ensure_max_dyn_smem((const void*)omega_sym_kernel, (size_t)((int)smem));
     if (e != cudaSuccess) return e;
     const int64_t b0 = jlo * (jlo + 1) / 2;
     const int64_t ctas = jhi * (jhi + 1) / 2 - b0;
