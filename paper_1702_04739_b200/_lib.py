@@ -106,6 +106,7 @@ SIGNATURES = {
     "isoc_tree_destroy": (None, [P]),
     "isoc_exp_dev": (ctypes.c_int, [P, P, I64, P]),
     "isoc_run": (ctypes.c_int, [P, I64, I32, I64, D, D, I64, P, ctypes.POINTER(RunOut)]),
+    "isoc_release_cached_memory": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
     "isoc_launch_count": (ctypes.c_longlong, []),
     "isoc_prof_enable": (None, [ctypes.c_int]),
     "isoc_prof_read": (ctypes.c_int, [ctypes.c_int, PD, ctypes.POINTER(ctypes.c_longlong)]),

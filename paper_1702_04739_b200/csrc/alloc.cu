@@ -21,6 +21,7 @@
 
 #include <cuda_runtime.h>
 
+#include "../../include/isoclust_b200.h"
 #include "common.cuh"
 
 namespace isoc {
@@ -137,3 +138,14 @@ cudaError_t isoc_free_async(void* p, cudaStream_t st) {
 }
 
 }  // namespace isoc
+
+extern "C" int isoc_release_cached_memory(unsigned long long* released_bytes_host) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return ISOC_ECUDA;
+    isoc::Cache& c = isoc::cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    const size_t before = c.cached;
+    isoc::evict_locked(c, dev, SIZE_MAX);
+    if (released_bytes_host) *released_bytes_host = (unsigned long long)(before - c.cached);
+    return ISOC_OK;
+}
