@@ -747,7 +747,8 @@ def main():
             "cpu_baseline": cpu,
             "parity": parity,
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "last_step_stage_ms": {kk: round(v, 2) for kk, v in run_h.timings_ms.items()}},
             "gpu_launches": int(launches),
             "clocks": clocks,
         }
