@@ -635,12 +635,12 @@ def main():
     executed_pairs = {}
     if world == 1:
         # sigma: 2048-wide super-blocks of 16 x 16 tiles of 128, waves planned
-        # as launch_sigma_sym_range does (40 GB of 1364-byte slots, >= 8
+        # as launch_sigma_sym_range does (64 GB of 1364-byte slots, >= 8
         # blocks); omega: 1024-wide super-blocks, no strip
         sb, nt = 2048, 16
         nbs = -(-n // sb)
         if n >= 2048:
-            budget = (40 << 30) // (32 * 8 + 20 + 136 * 8)
+            budget = (64 << 30) // (32 * 8 + 20 + 136 * 8)
             last = set()
             w0 = 0
             while w0 < nbs:
